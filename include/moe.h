@@ -1,0 +1,207 @@
+/*
+ * moe.h — C-ABI of the B200-native expert-cached MoE decode block
+ *         (arXiv 2512.16473, "Efficient CPU-GPU Collaborative Inference for
+ *          MoE-based LLMs on Memory-Limited Systems").
+ *
+ * One call of moe_layer_forward() is one pass of the paper's per-layer MoE block
+ * at single-request decode (Fig.4a):
+ *   router gating — gate GEMV, top-K, softmax over the K      (DESIGN R1/R2)
+ *   (1) cache check of the layer's set in the N x M cache
+ *   (3) LRU update; a missed expert is fetched from pinned host
+ *       memory into its victim slot on a side stream
+ *   (2a) SwiGLU expert FFN GEMVs over the (now) resident slots,
+ *        combined by the gate weights
+ *   tensor-parallel only: per-layer NCCL all-reduce of y        (north_star (4))
+ * Layers >= N (beyond coverage) take the miss path through a staging slot
+ * and are never inserted.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns moe_status; 0 == MOE_OK. No C++ exception crosses the ABI.
+ *    On a non-OK status moe_last_error() returns a thread-local message and the
+ *    context is left unchanged (arguments are validated before anything is enqueued).
+ *  - No torch types: plain host/device pointers, sizes, and a cudaStream_t passed
+ *    as void*. The library sets the context's CUDA device on entry.
+ *  - Single-threaded per context: calls on one ctx must not race, and all
+ *    moe_layer_forward calls of one ctx must be ordered on one stream.
+ *  - Decode batch = 1. bf16 values are passed as their uint16_t bit patterns.
+ */
+#ifndef MOE_H_
+#define MOE_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MOE_API __attribute__((visibility("default")))
+#else
+#define MOE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t moe_status;
+#define MOE_OK 0
+#define MOE_ERR_INVALID_ARG 1   /* bad pointer / size / index / geometry */
+#define MOE_ERR_OUT_OF_MEMORY 2 /* device or pinned-host allocation failed */
+#define MOE_ERR_CUDA 3          /* a CUDA runtime/driver call failed */
+#define MOE_ERR_NCCL 4          /* NCCL missing or an NCCL call failed */
+#define MOE_ERR_STATE 5         /* call out of order (e.g. forward before cache_configure) */
+#define MOE_ERR_UNSUPPORTED 6   /* valid but not implemented (e.g. a NEXT policy) */
+
+#define MOE_ABI_VERSION 1
+#define MOE_MAX_EXPERTS 32 /* n <= 32: one warp lane per expert / per way in the router kernel */
+
+typedef struct moe_ctx moe_ctx; /* opaque; created by moe_init, freed by moe_destroy */
+
+/* Model shape (Table II) and placement.
+ *  num_layers L >= 1; d_model d % 8 == 0; d_ff ff; num_experts n in [1, 32];
+ *  top_k K in [1, n]; device = CUDA ordinal.
+ *  tp_size P in {1, 2, 4, 8}: each expert's intermediate dimension is split across P
+ *  ranks (north_star (4)); ff % (8 * P) == 0; rank tp_rank holds rows
+ *  [tp_rank*ff/P, (tp_rank+1)*ff/P) of W1/W3 and the matching columns of W2.
+ *  nccl_unique_id: 128 bytes from moe_nccl_unique_id() on rank 0, broadcast by the
+ *  caller (e.g. torch.distributed); must be NULL iff tp_size == 1. */
+typedef struct {
+  int32_t num_layers, d_model, d_ff, num_experts, top_k;
+  int32_t device;
+  int32_t tp_size, tp_rank;
+  const uint8_t* nccl_unique_id;
+} moe_model_desc;
+
+/* Host backing store of ALL weights ("store model weights in CPU memory").
+ *  gate[l]          -> Wg of layer l, [n][d] bf16 row-major. Copied to the device at
+ *                      moe_init (router networks stay resident on the GPU).
+ *  expert_blob[l*n+e] -> this rank's slice of expert e of layer l, one contiguous blob
+ *                      of slot_bytes = 3*d*(ff/P)*2 bytes laid out as
+ *                      { W1[ff/P][d], W3[ff/P][d], W2[d][ff/P] } (nn.Linear layout).
+ *  All pointers are HOST pointers, CALLER-OWNED, and must outlive the ctx.
+ *  already_pinned: nonzero if the blobs are page-locked (cudaHostAlloc / torch
+ *  pin_memory); 0 -> the library cudaHostRegister()s them and unregisters in
+ *  moe_destroy. Copies from unpinned memory would not be asynchronous. */
+typedef struct {
+  const uint16_t* const* gate;
+  const uint16_t* const* expert_blob;
+  int32_t already_pinned;
+} moe_weights;
+
+/* Validates desc/weights, uploads the gate weights, pins the host blobs, creates the
+ * fetch stream (the weight channel of P:226's two streams), the miss-notification
+ * mailbox and, if tp_size > 1, the NCCL communicator (collective over the TP group:
+ * all ranks must call moe_init concurrently). *out receives the new context. */
+MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* weights, moe_ctx** out);
+
+/* Waits for all outstanding work, frees device memory, unpins, destroys the comm. NULL ok. */
+MOE_API moe_status moe_destroy(moe_ctx* ctx);
+
+typedef enum {
+  MOE_POLICY_LRU = 0,          /* P:217 (default; the paper's policy) */
+  MOE_POLICY_FIFO = 1,         /* P:218 compared policy: no recency update on a hit */
+  MOE_POLICY_STATIC_RANDOM = 2 /* P:360 analytic baseline: NEXT — returns MOE_ERR_UNSUPPORTED */
+} moe_policy;
+
+/* Cache geometry and policy.
+ *  cache_bytes >= 0: S = floor(cache_bytes / slot_bytes), N_raw = floor(S / M)
+ *                    (P:214), covered layers = min(N_raw, L) (set l <-> layer l, R7).
+ *  cache_bytes == -1: N = indexes directly (0 <= indexes <= L), S = N * M.
+ *  ways M: K <= M <= n (M < K is rejected, reading R12).
+ *  warm_start: 0 = cold (all ways invalid); 1 = experts 0..M-1 of every covered layer
+ *              preloaded into ways 0..M-1 with recency 1..M (blocking H2D; not counted
+ *              as fetches; reading R9).
+ *  pool/pool_bytes: optional caller-provided DEVICE memory for the slot pool (e.g. a
+ *              torch tensor), >= (covered*M + K) * slot_bytes; NULL -> cudaMalloc.
+ *              The K extra slots stage uncovered-layer experts.
+ *  Resets directory, recency clock, stats, trace and token counters. S == 0 is legal:
+ *  every layer is uncovered. Synchronizes the device. */
+typedef struct {
+  int64_t cache_bytes;
+  int32_t ways;
+  int32_t indexes;
+  int32_t policy;
+  int32_t warm_start;
+  uint64_t seed; /* STATIC_RANDOM only (NEXT) */
+  void* pool;
+  int64_t pool_bytes;
+} moe_cache_config;
+
+typedef struct {
+  int64_t slots_S, slot_bytes, pool_bytes;
+  int32_t ways_M, indexes_N_raw, covered_layers, reserved;
+} moe_cache_geometry;
+
+MOE_API moe_status cache_configure(moe_ctx* ctx, const moe_cache_config* cfg, moe_cache_geometry* out);
+
+/* One decode step of the MoE block of `layer` for one token.
+ *  x: DEVICE bf16 [d], caller-owned, ready on `stream` at call time.
+ *  y: DEVICE fp32 [d], caller-owned, fully overwritten (no residual added); valid once
+ *     `stream` reaches this point. TP: every rank passes the same x and gets the
+ *     all-reduced y.
+ *  stream: cudaStream_t (void*; NULL = legacy default stream).
+ * Enqueue-only: never synchronizes the host on the hit path. Calls MUST come in decode
+ * order (token-major, layer-ascending): call order defines LRU recency and the
+ * token index of each layer (its number of previous calls). Invalid layer ->
+ * MOE_ERR_INVALID_ARG and no cache mutation. Misses are filled on the fetch stream by a
+ * runtime thread; the expert kernels wait on the slot's ready generation. */
+MOE_API moe_status moe_layer_forward(moe_ctx* ctx, int32_t layer, const void* x, float* y, void* stream);
+
+/* End-to-end variant of moe_layer_forward with HOST buffers: copies x (bf16 [d], best
+ * pinned) host->device, runs the layer on the context's own stream, copies y (fp32 [d])
+ * device->host and synchronizes. */
+MOE_API moe_status moe_layer_forward_host(moe_ctx* ctx, int32_t layer, const uint16_t* x_host, float* y_host);
+
+/* Per-layer counters (Fig.6 hit-rate definitions; SPEC CacheStats S:203-207).
+ *  at_least_one_hit = the paper's "expert(s) hit"; all_k_hit = "2 experts hit" (K=2).
+ *  expert_misses includes coverage_misses (layers >= N). fetches / fetch_bytes count
+ *  host->device expert copies (one per miss, including staging fills).
+ *  hit_under_fill: hits on a slot whose fill had not landed yet at probe time (timing
+ *  dependent — not part of the bit-exact contract). */
+typedef struct {
+  uint64_t accesses, at_least_one_hit, all_k_hit, expert_hits, expert_misses, coverage_misses,
+      evictions, fetches, fetch_bytes, hit_under_fill;
+} moe_layer_stats;
+
+/* layer in [0, L) or -1 for the sum over layers. Synchronizes the context's streams. */
+MOE_API moe_status cache_stats(moe_ctx* ctx, int32_t layer, moe_layer_stats* out);
+
+/* One record per (token, layer, rank) in call order (SPEC trace vocabulary S:354).
+ *  way = -1 and coverage = 1 for layers beyond coverage; evicted = -1 if no eviction. */
+typedef struct {
+  uint32_t token;
+  uint16_t layer;
+  uint8_t rank, hit;
+  int16_t expert, evicted;
+  int8_t way;
+  uint8_t coverage;
+  uint16_t reserved;
+  float weight; /* gate weight w_r (fp32) */
+} moe_access_record;
+
+/* Copies up to cap records (oldest first) into host_out; *n_out = number recorded since
+ * cache_configure (may exceed the device ring capacity set by MOE_TRACE_CAP, default
+ * 2^20 records; records beyond it are dropped). Synchronizes. */
+MOE_API moe_status cache_trace(moe_ctx* ctx, moe_access_record* host_out, int64_t cap, int64_t* n_out);
+
+/* Kernel timing (diagnostics for the roofline report). When enabled, CUDA events are
+ * recorded around every kernel on the launch stream. moe_profile_read synchronizes and
+ * returns the accumulated device time (ms) and launch count per kernel class:
+ *  0 route_probe (router + cache kernel), 1 expert_ffn (the fused persistent expert
+ *  kernel; on the split fallback path: the gate/up kernel), 2 expert_down (split fallback
+ *  path only), 3 allreduce (TP). Reading resets. */
+#define MOE_PROF_KINDS 4
+typedef struct {
+  double ms[MOE_PROF_KINDS];
+  uint64_t launches[MOE_PROF_KINDS];
+} moe_profile_t;
+MOE_API moe_status moe_profile_enable(moe_ctx* ctx, int32_t enable);
+MOE_API moe_status moe_profile_read(moe_ctx* ctx, moe_profile_t* out);
+
+/* 128-byte NCCL unique id for a TP group (dlopens libnccl.so.2). */
+MOE_API moe_status moe_nccl_unique_id(uint8_t* out128);
+
+MOE_API const char* moe_last_error(void);
+MOE_API int32_t moe_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_H_ */

@@ -1,0 +1,103 @@
+// moe_internal.cuh — device-side records, kernel argument blocks and launchers
+// shared by the runtime (runtime.cu) and the sm_100a kernels (route_probe.cu,
+// expert_gemv.cu). Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "moe.h"
+
+namespace moe {
+
+constexpr int kMaxK = MOE_MAX_EXPERTS;  // K <= n <= 32
+constexpr int kMailRing = 1024;         // miss-notification mailbox entries (host-mapped)
+
+// Per-layer device counters, same order as moe_layer_stats.
+struct DevStats {
+  unsigned long long accesses, at_least_one_hit, all_k_hit, expert_hits, expert_misses,
+      coverage_misses, evictions, fetches, fetch_bytes, hit_under_fill;
+};
+static_assert(sizeof(DevStats) == sizeof(moe_layer_stats), "stats layout");
+
+// Routing decision of the current call, written by the router kernel and read by the
+// expert kernels on the same stream (stream order = no race).
+struct RouteRec {
+  int32_t K;
+  int32_t expert[kMaxK];
+  float w[kMaxK];
+  int32_t slot[kMaxK];   // slot index in the pool (cache way or staging slot)
+  uint32_t gen[kMaxK];   // fill generation the slot must reach before it is read
+};
+
+// One mailbox entry per call, in HOST-MAPPED pinned memory. The router kernel writes the
+// payload, fences (system scope), then publishes `seq`; the runtime's fetch thread polls
+// `seq` and issues the copies of the missed experts on the fetch stream.
+struct Mail {
+  volatile unsigned long long seq;
+  int32_t layer, nmiss;
+  int32_t expert[kMaxK];
+  int32_t slot[kMaxK];
+  uint32_t gen[kMaxK];
+};
+
+struct RouteArgs {
+  const uint16_t* Wg;  // [n][d] gate of this layer (device)
+  const uint16_t* x;   // [d] (device)
+  int d, n, K, M, layer, covered, policy;
+  int32_t* tag;        // [M] set of this layer (covered only)
+  unsigned long long* stamp;  // [M]
+  int slot_base;       // first slot of this layer's set (= layer * M)
+  int staging_base;    // first staging slot (= covered_layers * M)
+  uint32_t* gen;       // [slots + K] fill generation per slot
+  const uint32_t* ready;  // [slots + K] landed generation per slot (written by the fetch stream)
+  unsigned long long* clock;
+  DevStats* stats;     // &stats[layer]
+  RouteRec* route;
+  moe_access_record* trace;
+  long long trace_idx, trace_cap;
+  uint32_t token;
+  Mail* mail;          // device alias of the host-mapped ring entry for this call
+  unsigned long long seq;
+  long long slot_bytes;
+};
+
+struct ExpertArgs {
+  const RouteRec* route;
+  const uint8_t* pool;
+  long long slot_bytes;
+  const uint16_t* x;  // [d]
+  int d, ffr, K;
+  float* h;           // [K][ffr] SwiGLU activations (scratch)
+  float* y;           // [d]
+  const uint32_t* ready;
+};
+
+// Fused persistent expert kernel (expert_fused.cu).
+constexpr int kFusedMaxDynSmem = 232448 - 1024;  // 227 KB opt-in minus static shared memory
+struct FusedArgs {
+  ExpertArgs e;
+  unsigned long long* bar;        // grid-barrier counter (monotonic across calls)
+  unsigned long long bar_target;  // (call index + 1) * gridDim.x
+  int NS, SB;                     // ring stages / stage bytes
+  int xh_bytes, ypart_bytes;
+  unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
+};
+struct FusedPlan {
+  int SB, NS, xh_bytes, ypart_bytes, threads;
+  size_t smem;
+};
+bool plan_fused(int d, int ffr, int K, int grid, FusedPlan* p);
+cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl);
+cudaError_t preload_fused_kernels();
+
+cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl);
+void launch_expert_gateup(const ExpertArgs& a, cudaStream_t s, int num_sms);
+void launch_expert_down(const ExpertArgs& a, cudaStream_t s, int num_sms);
+void launch_write_ready(uint32_t* ready, int slot, uint32_t gen, cudaStream_t s);
+
+// Force-load every kernel of this library now (CUDA lazy loading would otherwise load a
+// kernel at its first launch; loading while another kernel spins on a flag can deadlock).
+cudaError_t preload_route_kernels();
+cudaError_t preload_expert_kernels();
+
+}  // namespace moe

@@ -1,0 +1,276 @@
+// route_probe.cu — K1: fused router + cache probe + on-device LRU update (sm_100a).
+//
+// One CTA per call. Warps compute the gate GEMV z = Wg x (16-byte loads, fp32
+// accumulation, warp-shuffle reduction). Warp 0 then does, with one lane per expert
+// and one lane per way:
+//   top-K by (z desc, index asc) and softmax over the K           (R1, R2)
+//   step 1 cache check of set `layer` against the pre-access state (R10)
+//   LRU restamp of hits, then victim/insert of misses in rank order,
+//   never evicting a way that holds an expert of this access       (R10)
+//   layers >= N: coverage misses into staging slots, no insertion   (R13)
+// and writes the route record (for the expert kernels), the access trace, the
+// per-layer counters and the miss mailbox (host-mapped; P:200's post-fetch is issued
+// by the runtime's fetch thread from it).
+#include <math.h>
+
+#include "moe_internal.cuh"
+#include "ptx.cuh"
+
+namespace moe {
+namespace {
+
+using ptx::griddep_launch_dependents;
+using ptx::griddep_wait;
+
+__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+__device__ __forceinline__ float dot8_bf16(const int4 a, const int4 b) {
+  float s = bf_lo(a.x) * bf_lo(b.x);
+  s = fmaf(bf_hi(a.x), bf_hi(b.x), s);
+  s = fmaf(bf_lo(a.y), bf_lo(b.y), s);
+  s = fmaf(bf_hi(a.y), bf_hi(b.y), s);
+  s = fmaf(bf_lo(a.z), bf_lo(b.z), s);
+  s = fmaf(bf_hi(a.z), bf_hi(b.z), s);
+  s = fmaf(bf_lo(a.w), bf_lo(b.w), s);
+  s = fmaf(bf_hi(a.w), bf_hi(b.w), s);
+  return s;
+}
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+constexpr int kPF = 8;  // gate chunks per lane prefetched into registers before the PDL wait
+
+__global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a) {
+  __shared__ float part[MOE_MAX_EXPERTS][kWarps + 1];
+  __shared__ int sS[kMaxK];
+  __shared__ float sZ[kMaxK], sW[kMaxK];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- gate GEMV z = Wg x: G = 32/n warps per expert row, lane-strided 16-B chunks.
+  // The gate rows do not depend on x, so they are loaded BEFORE griddepcontrol.wait and
+  // overlap the tail of the preceding kernel (programmatic dependent launch).
+  const int n = a.n;
+  const int G = kWarps / n;                 // n <= 32 -> G >= 1
+  const int e = warp / G, g = warp - e * G;
+  const bool active = e < n;
+  const int nchunk = a.d >> 3;
+  const int stride = 32 * G;
+  const int c0 = g * 32 + lane;
+  const int4* wr = reinterpret_cast<const int4*>(a.Wg + (size_t)(active ? e : 0) * a.d);
+  int4 wv[kPF];
+#pragma unroll
+  for (int k = 0; k < kPF; ++k) {
+    const int c = c0 + k * stride;
+    if (active && c < nchunk) wv[k] = __ldg(wr + c);
+  }
+  griddep_launch_dependents();  // let the expert kernel's CTAs get resident early
+  griddep_wait();               // x and the previous calls' directory writes are visible now
+  const int4* xv = reinterpret_cast<const int4*>(a.x);
+  float acc = 0.f;
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) {
+      const int c = c0 + k * stride;
+      if (c < nchunk) acc += dot8_bf16(wv[k], __ldg(xv + c));
+    }
+    for (int c = c0 + kPF * stride; c < nchunk; c += stride) acc += dot8_bf16(__ldg(wr + c), __ldg(xv + c));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0 && active) part[e][g] = acc;
+  __syncthreads();
+  if (warp != 0) return;
+  float zsum = 0.f;
+  if (lane < n)
+    for (int q = 0; q < G; ++q) zsum += part[lane][q];  // fixed order: deterministic
+
+  const int K = a.K, M = a.M;
+  // ---- top-K: K rounds of warp argmax, ties -> lower expert index
+  const float z = lane < n ? zsum : -INFINITY;
+  bool taken = lane >= n;
+  for (int r = 0; r < K; ++r) {
+    float v = taken ? -INFINITY : z;
+    int idx = taken ? 0x7fffffff : lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    if (lane == idx) taken = true;
+    if (lane == 0) { sS[r] = idx; sZ[r] = v; }
+  }
+  __syncwarp();
+  // ---- softmax over the K selected logits (rank order, fp32)
+  if (lane == 0) {
+    const float m = sZ[0];
+    float sum = 0.f;
+    for (int r = 0; r < K; ++r) { sW[r] = expf(sZ[r] - m); sum += sW[r]; }
+    for (int r = 0; r < K; ++r) sW[r] = sW[r] / sum;
+  }
+  __syncwarp();
+
+  // ---- cache probe + LRU update (lane = way)
+  int myS = lane < K ? sS[lane] : -1;  // lane r < K carries rank r's decision
+  int myHit = 0, myWay = -1, myEv = -1, mySlot = 0;
+  uint32_t myGen = 0;
+  unsigned long long clock = 0;
+  int nhit = 0, nev = 0, huf = 0;
+  if (a.covered) {
+    int32_t tag = lane < M ? a.tag[lane] : -2;
+    unsigned long long st = lane < M ? a.stamp[lane] : 0ull;
+    uint32_t gen = lane < M ? a.gen[a.slot_base + lane] : 0u;
+    clock = *a.clock;
+    // step 1: partition against the pre-access state
+    for (int r = 0; r < K; ++r) {
+      const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sS[r]);
+      if (lane == r) { myHit = m != 0u; myWay = m ? __ffs(m) - 1 : -1; }
+    }
+    // step 2: touch hits in rank order (LRU; FIFO keeps insertion order)
+    for (int r = 0; r < K; ++r) {
+      const int h = __shfl_sync(0xffffffffu, myHit, r);
+      const int w = __shfl_sync(0xffffffffu, myWay, r);
+      if (h && a.policy == MOE_POLICY_LRU) {
+        ++clock;
+        if (lane == w) st = clock;
+      }
+    }
+    // step 3: insert misses in rank order
+    for (int r = 0; r < K; ++r) {
+      if (__shfl_sync(0xffffffffu, myHit, r)) continue;
+      const unsigned inval = __ballot_sync(0xffffffffu, lane < M && tag == -1);
+      int v;
+      if (inval) {
+        v = __ffs(inval) - 1;
+      } else {
+        bool pinned = false;
+        for (int q = 0; q < K; ++q) pinned |= (tag == sS[q]);
+        const bool cand = lane < M && !pinned;
+        unsigned long long key = cand ? st : ~0ull;
+        int kl = cand ? lane : 64;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, kl, o);
+          if (ok < key || (ok == key && ol < kl)) { key = ok; kl = ol; }
+        }
+        v = kl;
+      }
+      const int ev = __shfl_sync(0xffffffffu, tag, v);
+      ++clock;
+      if (lane == v) { tag = sS[r]; st = clock; ++gen; }
+      if (lane == r) { myWay = v; myEv = ev; }
+    }
+    // write the set back; per-rank slot / generation
+    if (lane < M) {
+      a.tag[lane] = tag;
+      a.stamp[lane] = st;
+      a.gen[a.slot_base + lane] = gen;
+    }
+    const int wq = myWay < 0 ? 0 : myWay;
+    const uint32_t g = __shfl_sync(0xffffffffu, gen, wq);
+    if (lane < K) {
+      mySlot = a.slot_base + myWay;
+      myGen = g;
+      if (myHit) {
+        const uint32_t rd = *((volatile const uint32_t*)(a.ready + mySlot));
+        huf = rd < g;
+      }
+    }
+  } else {
+    // beyond coverage: every expert is fetched into a staging slot, never inserted
+    if (lane < K) {
+      mySlot = a.staging_base + lane;
+      myGen = a.gen[mySlot] + 1u;
+      a.gen[mySlot] = myGen;
+    }
+  }
+  nhit = __popc(__ballot_sync(0xffffffffu, lane < K && myHit));
+  nev = __popc(__ballot_sync(0xffffffffu, lane < K && myEv >= 0));
+  huf = __popc(__ballot_sync(0xffffffffu, lane < K && huf));
+  const unsigned missmask = __ballot_sync(0xffffffffu, lane < K && !myHit);
+
+  // ---- route record, trace, mailbox
+  if (lane < K) {
+    a.route->expert[lane] = myS;
+    a.route->w[lane] = sW[lane];
+    a.route->slot[lane] = mySlot;
+    a.route->gen[lane] = myGen;
+    if (a.trace_idx + lane < a.trace_cap) {
+      moe_access_record rec;
+      rec.token = a.token;
+      rec.layer = (uint16_t)a.layer;
+      rec.rank = (uint8_t)lane;
+      rec.hit = (uint8_t)myHit;
+      rec.expert = (int16_t)myS;
+      rec.evicted = (int16_t)myEv;
+      rec.way = (int8_t)myWay;
+      rec.coverage = (uint8_t)(!a.covered);
+      rec.reserved = 0;
+      rec.weight = sW[lane];
+      a.trace[a.trace_idx + lane] = rec;
+    }
+    if (!myHit) {
+      const int i = __popc(missmask & ((1u << lane) - 1u));
+      a.mail->expert[i] = myS;
+      a.mail->slot[i] = mySlot;
+      a.mail->gen[i] = myGen;
+    }
+  }
+  if (lane == 0) {
+    a.route->K = K;
+    if (a.covered) *a.clock = clock;
+    DevStats* s = a.stats;
+    const int nmiss = K - nhit;
+    s->accesses += 1;
+    s->at_least_one_hit += nhit > 0;
+    s->all_k_hit += nhit == K;
+    s->expert_hits += nhit;
+    s->expert_misses += nmiss;
+    s->coverage_misses += a.covered ? 0 : K;
+    s->evictions += nev;
+    s->fetches += nmiss;
+    s->fetch_bytes += (unsigned long long)nmiss * (unsigned long long)a.slot_bytes;
+    s->hit_under_fill += huf;
+    a.mail->layer = a.layer;
+    a.mail->nmiss = nmiss;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_system();
+    a.mail->seq = a.seq;  // publish (volatile store to host-mapped memory)
+  }
+}
+
+__global__ void write_ready_kernel(uint32_t* ready, int slot, uint32_t gen) {
+  *((volatile uint32_t*)(ready + slot)) = gen;
+}
+
+}  // namespace
+
+cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, route_probe_kernel, a);
+}
+
+cudaError_t preload_route_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, route_probe_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, write_ready_kernel);
+  return e;
+}
+
+void launch_write_ready(uint32_t* ready, int slot, uint32_t gen, cudaStream_t s) {
+  write_ready_kernel<<<1, 1, 0, s>>>(ready, slot, gen);
+}
+
+}  // namespace moe

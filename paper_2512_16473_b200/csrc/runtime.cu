@@ -1,0 +1,714 @@
+// runtime.cu — host runtime behind the C-ABI (include/moe.h).
+//
+// Owns: device copy of the router gates, the expert slot pool and its directory
+// (tag / recency stamp per way, fill generation and landed generation per slot), the
+// per-layer counters and access trace, the fetch stream (P:226's weight channel), a
+// host-mapped miss mailbox and the fetch thread that turns mailbox entries into
+// H2D copies + ready-generation writes, optional NCCL communicator for the
+// ff-split (north_star (4)), and per-kernel profiling events.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <string.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "moe_internal.cuh"
+#include "nccl.h"
+
+using namespace moe;
+
+// ----------------------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static moe_status fail(moe_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? MOE_ERR_OUT_OF_MEMORY : MOE_ERR_CUDA, \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+static std::mutex g_nccl_mu;
+
+static bool nccl_load(std::string* why) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.h) return true;
+  const char* env = getenv("MOE_NCCL_LIB");
+  void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    *why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+    return false;
+  }
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy) {
+    *why = "libnccl.so.2 lacks required symbols";
+    dlclose(h);
+    return false;
+  }
+  g_nccl.h = h;
+  return true;
+}
+
+// ----------------------------------------------------------------------------- context
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct ProfEv {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+struct moe_ctx {
+  // shape
+  int L = 0, d = 0, ff = 0, n = 0, K = 0, P = 1, rank = 0, ffr = 0, device = 0;
+  long long slot_bytes = 0;
+  int num_sms = 0;
+  // weights
+  std::vector<const uint16_t*> blobs;
+  std::vector<void*> registered;
+  uint16_t* d_gate = nullptr;
+  // streams
+  cudaStream_t fetch_stream = nullptr, own_stream = nullptr;
+  PFN_writeValue32 write_value32 = nullptr;
+  // cache
+  bool configured = false;
+  int M = 0, Ncov = 0, Nraw = 0, policy = 0;
+  long long S = 0, nslots = 0;
+  uint8_t* pool = nullptr;
+  bool pool_owned = false;
+  long long pool_bytes = 0;
+  int32_t* d_tag = nullptr;
+  unsigned long long* d_stamp = nullptr;
+  uint32_t* d_gen = nullptr;
+  uint32_t* d_ready = nullptr;
+  unsigned long long* d_clock = nullptr;
+  DevStats* d_stats = nullptr;
+  RouteRec* d_route = nullptr;
+  float* d_h = nullptr;
+  moe_access_record* d_trace = nullptr;
+  long long trace_cap = 0, trace_count = 0;
+  std::vector<uint32_t> tokens;  // per-layer call count = token index
+  // mailbox + fetch thread
+  Mail* h_mail = nullptr;
+  Mail* d_mail = nullptr;
+  std::atomic<unsigned long long> issued{0}, consumed{0};
+  std::atomic<bool> stop{false};
+  std::atomic<int> fetch_error{0};
+  std::string fetch_error_msg;
+  std::thread fetcher;
+  // end-to-end buffers
+  uint16_t* d_x_e2e = nullptr;
+  float* d_y_e2e = nullptr;
+  // profiling
+  bool prof = false;
+  std::vector<ProfEv> prof_events;
+  std::vector<cudaEvent_t> ev_free;
+  double prof_ms[MOE_PROF_KINDS] = {0, 0, 0, 0};
+  uint64_t prof_launches[MOE_PROF_KINDS] = {0, 0, 0, 0};
+  cudaEvent_t done_ev = nullptr;
+  bool any_call = false;
+  // TP
+  ncclComm_t comm = nullptr;
+  // fused persistent expert kernel
+  bool fused = false, pdl = true;
+  FusedPlan plan{};
+  int fused_grid = 0;
+  unsigned long long* d_bar = nullptr;
+  unsigned long long fused_calls = 0;
+  unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
+  unsigned* d_dbg = nullptr;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void fetch_thread_main(moe_ctx* c) {
+  cudaSetDevice(c->device);
+  const char* dly = getenv("MOE_DEBUG_FETCH_DELAY_US");  // fault injection (tests only)
+  const long delay_us = dly ? atol(dly) : 0;
+  const bool log = getenv("MOE_DEBUG_FETCH_LOG") != nullptr;
+  unsigned long long next = c->consumed.load() + 1;
+  auto idle_since = std::chrono::steady_clock::now();
+  while (true) {
+    if (next > c->issued.load(std::memory_order_acquire)) {
+      if (c->stop.load()) break;
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+      continue;
+    }
+    Mail* m = &c->h_mail[next % kMailRing];
+    int spins = 0;
+    idle_since = std::chrono::steady_clock::now();
+    bool abandoned = false;
+    while (m->seq != next) {
+      if (++spins > 2000) std::this_thread::sleep_for(std::chrono::microseconds(10));
+      if (c->stop.load() &&
+          std::chrono::steady_clock::now() - idle_since > std::chrono::seconds(5)) {
+        abandoned = true;
+        break;
+      }
+    }
+    if (abandoned) break;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const int layer = m->layer, nmiss = m->nmiss;
+    for (int i = 0; i < nmiss; ++i) {
+      const int slot = m->slot[i];
+      const int e = m->expert[i];
+      const uint32_t gen = m->gen[i];
+      if (delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(delay_us));
+      if (log) fprintf(stderr, "[moe fetch] seq=%llu layer=%d expert=%d slot=%d gen=%u\n", next, layer, e, slot, gen);
+      cudaError_t err = cudaMemcpyAsync(c->pool + (long long)slot * c->slot_bytes,
+                                        c->blobs[(size_t)layer * c->n + e], (size_t)c->slot_bytes,
+                                        cudaMemcpyHostToDevice, c->fetch_stream);
+      CUresult cr = CUDA_SUCCESS;
+      if (err == cudaSuccess) {
+        if (c->write_value32)
+          cr = c->write_value32((CUstream)c->fetch_stream, (CUdeviceptr)(c->d_ready + slot), gen, 0);
+        else
+          launch_write_ready(c->d_ready, slot, gen, c->fetch_stream);
+      }
+      if ((err != cudaSuccess || cr != CUDA_SUCCESS) && !c->fetch_error.load()) {
+        c->fetch_error_msg = std::string("fetch: ") + cudaGetErrorString(err);
+        c->fetch_error.store(1);
+      }
+    }
+    c->consumed.store(next, std::memory_order_release);
+    ++next;
+  }
+}
+
+cudaEvent_t prof_event(moe_ctx* c) {
+  if (!c->ev_free.empty()) {
+    cudaEvent_t e = c->ev_free.back();
+    c->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(moe_ctx* c, int kind, cudaStream_t s, ProfEv* pe) {
+  if (!c->prof) return;
+  pe->kind = kind;
+  pe->a = prof_event(c);
+  pe->b = prof_event(c);
+  cudaEventRecord(pe->a, s);
+}
+
+void prof_end(moe_ctx* c, cudaStream_t s, ProfEv* pe) {
+  if (!c->prof) return;
+  cudaEventRecord(pe->b, s);
+  c->prof_events.push_back(*pe);
+  if (c->prof_events.size() > 65536) {  // fold to bound memory
+    for (auto& p : c->prof_events) {
+      float ms = 0;
+      cudaEventSynchronize(p.b);
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      c->prof_ms[p.kind] += ms;
+      c->prof_launches[p.kind] += 1;
+      c->ev_free.push_back(p.a);
+      c->ev_free.push_back(p.b);
+    }
+    c->prof_events.clear();
+  }
+}
+
+void free_cache(moe_ctx* c) {
+  if (c->pool_owned && c->pool) cudaFree(c->pool);
+  c->pool = nullptr;
+  c->pool_owned = false;
+  cudaFree(c->d_tag);
+  cudaFree(c->d_stamp);
+  cudaFree(c->d_gen);
+  cudaFree(c->d_ready);
+  cudaFree(c->d_clock);
+  cudaFree(c->d_stats);
+  cudaFree(c->d_trace);
+  c->d_tag = nullptr;
+  c->d_stamp = nullptr;
+  c->d_gen = nullptr;
+  c->d_ready = nullptr;
+  c->d_clock = nullptr;
+  c->d_stats = nullptr;
+  c->d_trace = nullptr;
+  c->configured = false;
+}
+
+// Wait until every issued call's mailbox was consumed and the fetch stream drained.
+moe_status drain(moe_ctx* c) {
+  if (c->any_call) CUDA_TRY(cudaEventSynchronize(c->done_ev));
+  while (c->consumed.load(std::memory_order_acquire) < c->issued.load()) std::this_thread::yield();
+  CUDA_TRY(cudaStreamSynchronize(c->fetch_stream));
+  if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
+  return MOE_OK;
+}
+
+}  // namespace
+
+// ============================================================================= ABI
+extern "C" {
+
+MOE_API const char* moe_last_error(void) { return g_err.c_str(); }
+MOE_API int32_t moe_abi_version(void) { return MOE_ABI_VERSION; }
+
+// Debug only (not in moe.h): host pointer to the mapped kernel progress words, or NULL.
+MOE_API const unsigned* moe_debug_words(moe_ctx* c) { return c ? c->h_dbg : nullptr; }
+
+MOE_API moe_status moe_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return fail(MOE_ERR_INVALID_ARG, "out128 is NULL");
+  std::string why;
+  if (!nccl_load(&why)) return fail(MOE_ERR_NCCL, why);
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(MOE_ERR_NCCL, "ncclGetUniqueId failed");
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(out128, &id, 128);
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, moe_ctx** out) {
+  if (!desc || !w || !out) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  const int L = desc->num_layers, d = desc->d_model, ff = desc->d_ff, n = desc->num_experts,
+            K = desc->top_k, P = desc->tp_size, rank = desc->tp_rank;
+  if (L < 1 || d < 8 || d % 8 || ff < 8 || n < 1 || n > MOE_MAX_EXPERTS || K < 1 || K > n)
+    return fail(MOE_ERR_INVALID_ARG, "bad shape (need L>=1, d%8==0, 1<=K<=n<=32)");
+  if (!(P == 1 || P == 2 || P == 4 || P == 8) || rank < 0 || rank >= P || ff % (8 * P))
+    return fail(MOE_ERR_INVALID_ARG, "bad tensor-parallel split (P in {1,2,4,8}, ff % (8P) == 0)");
+  if ((P == 1) != (desc->nccl_unique_id == nullptr))
+    return fail(MOE_ERR_INVALID_ARG, "nccl_unique_id must be NULL iff tp_size == 1");
+  if (!w->gate || !w->expert_blob) return fail(MOE_ERR_INVALID_ARG, "NULL weight table");
+  for (int l = 0; l < L; ++l)
+    if (!w->gate[l]) return fail(MOE_ERR_INVALID_ARG, "NULL gate pointer");
+  for (int i = 0; i < L * n; ++i)
+    if (!w->expert_blob[i]) return fail(MOE_ERR_INVALID_ARG, "NULL expert blob pointer");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (desc->device < 0 || desc->device >= ndev) return fail(MOE_ERR_INVALID_ARG, "bad device ordinal");
+  DeviceGuard g(desc->device);
+
+  moe_ctx* c = new moe_ctx();
+  c->L = L; c->d = d; c->ff = ff; c->n = n; c->K = K; c->P = P; c->rank = rank;
+  c->ffr = ff / P; c->device = desc->device;
+  c->slot_bytes = 3ll * d * c->ffr * 2;
+  c->tokens.assign(L, 0);
+  auto bail = [&](moe_status st) {
+    moe_destroy(c);
+    return st;
+  };
+  cudaError_t e;
+#define INIT_TRY(expr)                                                                  \
+  do {                                                                                  \
+    e = (expr);                                                                         \
+    if (e != cudaSuccess)                                                               \
+      return bail(fail(e == cudaErrorMemoryAllocation ? MOE_ERR_OUT_OF_MEMORY : MOE_ERR_CUDA, \
+                       std::string(#expr) + ": " + cudaGetErrorString(e)));             \
+  } while (0)
+  INIT_TRY(preload_route_kernels());
+  INIT_TRY(preload_expert_kernels());
+  INIT_TRY(preload_fused_kernels());
+  INIT_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  c->blobs.assign(w->expert_blob, w->expert_blob + (size_t)L * n);
+  if (!w->already_pinned) {
+    for (auto* b : c->blobs) {
+      e = cudaHostRegister((void*)b, (size_t)c->slot_bytes, cudaHostRegisterDefault);
+      if (e == cudaSuccess) c->registered.push_back((void*)b);
+      else if (e == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();
+      else return bail(fail(MOE_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e)));
+    }
+  }
+  const size_t gate_elems = (size_t)n * d;
+  INIT_TRY(cudaMalloc(&c->d_gate, gate_elems * 2 * L));
+  for (int l = 0; l < L; ++l)
+    INIT_TRY(cudaMemcpy(c->d_gate + gate_elems * l, w->gate[l], gate_elems * 2, cudaMemcpyHostToDevice));
+  INIT_TRY(cudaStreamCreateWithFlags(&c->fetch_stream, cudaStreamNonBlocking));
+  INIT_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  INIT_TRY(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
+  INIT_TRY(cudaHostAlloc((void**)&c->h_mail, sizeof(Mail) * kMailRing, cudaHostAllocMapped));
+  memset((void*)c->h_mail, 0, sizeof(Mail) * kMailRing);
+  INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_mail, c->h_mail, 0));
+  INIT_TRY(cudaMalloc(&c->d_route, sizeof(RouteRec)));
+  INIT_TRY(cudaMalloc(&c->d_h, sizeof(float) * (size_t)K * c->ffr));
+  INIT_TRY(cudaMalloc(&c->d_x_e2e, sizeof(uint16_t) * d));
+  INIT_TRY(cudaMalloc(&c->d_y_e2e, sizeof(float) * d));
+  INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long)));
+  INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long)));
+  {
+    const char* path = getenv("MOE_EXPERT_PATH");
+    const char* pdl = getenv("MOE_PDL");
+    c->pdl = !(pdl && pdl[0] == '0');
+    c->fused_grid = c->num_sms;
+    c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, K, c->fused_grid, &c->plan);
+    if (getenv("MOE_DEBUG_KERNEL")) {
+      INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
+      memset(c->h_dbg, 0, 64);
+      INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_dbg, c->h_dbg, 0));
+      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d xh=%d ypart=%d smem=%zu grid=%d\n", (int)c->fused,
+              c->plan.NS, c->plan.SB, c->plan.xh_bytes, c->plan.ypart_bytes, c->plan.smem, c->fused_grid);
+    }
+  }
+  {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &fn, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      c->write_value32 = (PFN_writeValue32)fn;
+    cudaGetLastError();
+    if (getenv("MOE_DEBUG_FETCH_LOG"))
+      fprintf(stderr, "[moe init] cuStreamWriteValue32 %s\n", c->write_value32 ? "available" : "MISSING");
+  }
+  if (P > 1) {
+    std::string why;
+    if (!nccl_load(&why)) return bail(fail(MOE_ERR_NCCL, why));
+    ncclUniqueId id;
+    memcpy(&id, desc->nccl_unique_id, sizeof(id));
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, P, id, rank);
+    if (r != ncclSuccess) {
+      c->comm = nullptr;
+      return bail(fail(MOE_ERR_NCCL, std::string("ncclCommInitRank: ") +
+                                         (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?")));
+    }
+  }
+#undef INIT_TRY
+  c->fetcher = std::thread(fetch_thread_main, c);
+  *out = c;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_destroy(moe_ctx* c) {
+  if (!c) return MOE_OK;
+  DeviceGuard g(c->device);
+  if (c->any_call) cudaEventSynchronize(c->done_ev);
+  c->stop.store(true);
+  if (c->fetcher.joinable()) c->fetcher.join();
+  if (c->fetch_stream) cudaStreamSynchronize(c->fetch_stream);
+  for (auto& p : c->prof_events) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->ev_free) cudaEventDestroy(e);
+  free_cache(c);
+  cudaFree(c->d_gate);
+  cudaFree(c->d_route);
+  cudaFree(c->d_h);
+  cudaFree(c->d_x_e2e);
+  cudaFree(c->d_y_e2e);
+  cudaFree(c->d_bar);
+  if (c->h_mail) cudaFreeHost(c->h_mail);
+  for (void* p : c->registered) cudaHostUnregister(p);
+  if (c->done_ev) cudaEventDestroy(c->done_ev);
+  if (c->fetch_stream) cudaStreamDestroy(c->fetch_stream);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  cudaGetLastError();
+  delete c;
+  return MOE_OK;
+}
+
+MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_cache_geometry* out) {
+  if (!c || !cfg) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  DeviceGuard g(c->device);
+  const int M = cfg->ways;
+  if (M < c->K || M > c->n) return fail(MOE_ERR_INVALID_ARG, "ways must satisfy K <= M <= n");
+  if (cfg->policy == MOE_POLICY_STATIC_RANDOM)
+    return fail(MOE_ERR_UNSUPPORTED, "STATIC_RANDOM policy is not implemented (NEXT f1)");
+  if (cfg->policy != MOE_POLICY_LRU && cfg->policy != MOE_POLICY_FIFO)
+    return fail(MOE_ERR_INVALID_ARG, "unknown policy");
+  long long S;
+  int Nraw;
+  if (cfg->cache_bytes >= 0) {
+    S = cfg->cache_bytes / c->slot_bytes;
+    Nraw = (int)(S / M);
+  } else if (cfg->cache_bytes == -1) {
+    if (cfg->indexes < 0 || cfg->indexes > c->L) return fail(MOE_ERR_INVALID_ARG, "indexes out of [0, L]");
+    Nraw = cfg->indexes;
+    S = (long long)Nraw * M;
+  } else {
+    return fail(MOE_ERR_INVALID_ARG, "cache_bytes must be >= 0 or -1");
+  }
+  const int Ncov = Nraw < c->L ? Nraw : c->L;
+  const long long nslots = (long long)Ncov * M + c->K;  // + K staging slots
+  const long long need = nslots * c->slot_bytes;
+  if (cfg->pool && cfg->pool_bytes < need)
+    return fail(MOE_ERR_INVALID_ARG, "caller pool too small: need " + std::to_string(need) + " bytes");
+  moe_status st = drain(c);
+  if (st != MOE_OK) return st;
+  free_cache(c);
+  if (cfg->pool) {
+    c->pool = (uint8_t*)cfg->pool;
+    c->pool_owned = false;
+  } else {
+    cudaError_t e = cudaMalloc(&c->pool, (size_t)need);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      c->pool = nullptr;
+      return fail(MOE_ERR_OUT_OF_MEMORY, "slot pool cudaMalloc(" + std::to_string(need) + ") failed");
+    }
+    c->pool_owned = true;
+  }
+  c->M = M; c->Ncov = Ncov; c->Nraw = Nraw; c->S = S; c->nslots = nslots;
+  c->policy = cfg->policy; c->pool_bytes = need;
+  const long long nways = (long long)(Ncov > 0 ? Ncov : 1) * M;
+  CUDA_TRY(cudaMalloc(&c->d_tag, sizeof(int32_t) * nways));
+  CUDA_TRY(cudaMalloc(&c->d_stamp, sizeof(unsigned long long) * nways));
+  CUDA_TRY(cudaMalloc(&c->d_gen, sizeof(uint32_t) * nslots));
+  CUDA_TRY(cudaMalloc(&c->d_ready, sizeof(uint32_t) * nslots));
+  CUDA_TRY(cudaMalloc(&c->d_clock, sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&c->d_stats, sizeof(DevStats) * c->L));
+  const char* tc = getenv("MOE_TRACE_CAP");
+  c->trace_cap = tc ? atoll(tc) : (1ll << 20);
+  if (c->trace_cap < 0) c->trace_cap = 0;
+  CUDA_TRY(cudaMalloc(&c->d_trace, sizeof(moe_access_record) * (c->trace_cap > 0 ? c->trace_cap : 1)));
+  // directory: cold = all invalid; warm = experts 0..M-1 in ways 0..M-1, stamps 1..M (R9)
+  std::vector<int32_t> tag(nways, -1);
+  std::vector<unsigned long long> stamp(nways, 0);
+  std::vector<uint32_t> gen(nslots, 0);
+  unsigned long long clock = 0;
+  if (cfg->warm_start) {
+    for (int s = 0; s < Ncov; ++s)
+      for (int wy = 0; wy < M; ++wy) {
+        tag[(size_t)s * M + wy] = wy;
+        stamp[(size_t)s * M + wy] = wy + 1;
+        gen[(size_t)s * M + wy] = 1;
+        CUDA_TRY(cudaMemcpyAsync(c->pool + ((long long)s * M + wy) * c->slot_bytes,
+                                 c->blobs[(size_t)s * c->n + wy], (size_t)c->slot_bytes,
+                                 cudaMemcpyHostToDevice, c->fetch_stream));
+      }
+    clock = M;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_tag, tag.data(), sizeof(int32_t) * nways, cudaMemcpyHostToDevice, c->fetch_stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_stamp, stamp.data(), sizeof(unsigned long long) * nways, cudaMemcpyHostToDevice, c->fetch_stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_gen, gen.data(), sizeof(uint32_t) * nslots, cudaMemcpyHostToDevice, c->fetch_stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_ready, gen.data(), sizeof(uint32_t) * nslots, cudaMemcpyHostToDevice, c->fetch_stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_clock, &clock, sizeof(clock), cudaMemcpyHostToDevice, c->fetch_stream));
+  CUDA_TRY(cudaMemsetAsync(c->d_stats, 0, sizeof(DevStats) * c->L, c->fetch_stream));
+  CUDA_TRY(cudaStreamSynchronize(c->fetch_stream));
+  CUDA_TRY(cudaDeviceSynchronize());
+  c->trace_count = 0;
+  std::fill(c->tokens.begin(), c->tokens.end(), 0u);
+  c->configured = true;
+  if (out) {
+    out->slots_S = S;
+    out->slot_bytes = c->slot_bytes;
+    out->pool_bytes = need;
+    out->ways_M = M;
+    out->indexes_N_raw = Nraw;
+    out->covered_layers = Ncov;
+    out->reserved = 0;
+  }
+  return MOE_OK;
+}
+
+static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* y, cudaStream_t s) {
+  if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
+  if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
+  if (!x || !y) return fail(MOE_ERR_INVALID_ARG, "NULL x or y");
+  if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(MOE_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
+  if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
+  // host-side back-pressure: never let the GPU overwrite an unconsumed mailbox entry
+  const unsigned long long seq = c->issued.load() + 1;
+  while (seq - c->consumed.load(std::memory_order_acquire) >= (unsigned long long)kMailRing - 1)
+    std::this_thread::yield();
+  const bool covered = layer < c->Ncov;
+  RouteArgs ra;
+  ra.Wg = c->d_gate + (size_t)layer * c->n * c->d;
+  ra.x = (const uint16_t*)x;
+  ra.d = c->d; ra.n = c->n; ra.K = c->K; ra.M = c->M; ra.layer = layer;
+  ra.covered = covered; ra.policy = c->policy;
+  ra.tag = covered ? c->d_tag + (size_t)layer * c->M : nullptr;
+  ra.stamp = covered ? c->d_stamp + (size_t)layer * c->M : nullptr;
+  ra.slot_base = covered ? layer * c->M : 0;
+  ra.staging_base = c->Ncov * c->M;
+  ra.gen = c->d_gen;
+  ra.ready = c->d_ready;
+  ra.clock = c->d_clock;
+  ra.stats = c->d_stats + layer;
+  ra.route = c->d_route;
+  ra.trace = c->d_trace;
+  ra.trace_idx = c->trace_count;
+  ra.trace_cap = c->trace_cap;
+  ra.token = c->tokens[layer];
+  ra.mail = c->d_mail + (seq % kMailRing);
+  ra.seq = seq;
+  ra.slot_bytes = c->slot_bytes;
+
+  ExpertArgs ea;
+  ea.route = c->d_route;
+  ea.pool = c->pool;
+  ea.slot_bytes = c->slot_bytes;
+  ea.x = (const uint16_t*)x;
+  ea.d = c->d; ea.ffr = c->ffr; ea.K = c->K;
+  ea.h = c->d_h;
+  ea.y = y;
+  ea.ready = c->d_ready;
+
+  ProfEv pe;
+  prof_begin(c, 0, s, &pe);
+  CUDA_TRY(launch_route_probe(ra, s, c->pdl));
+  prof_end(c, s, &pe);
+  c->issued.store(seq, std::memory_order_release);  // the fetch thread may now wait for it
+  c->tokens[layer] += 1;
+  c->trace_count += c->K;
+  if (c->fused) {
+    FusedArgs fa;
+    fa.e = ea;
+    fa.bar = c->d_bar;
+    fa.bar_target = (c->fused_calls + 1) * (unsigned long long)c->fused_grid;
+    fa.NS = c->plan.NS;
+    fa.SB = c->plan.SB;
+    fa.xh_bytes = c->plan.xh_bytes;
+    fa.ypart_bytes = c->plan.ypart_bytes;
+    fa.dbg = c->d_dbg;
+    prof_begin(c, 1, s, &pe);
+    cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl);
+    if (e != cudaSuccess && c->pdl) {  // cooperative + PDL not accepted: retry without PDL
+      cudaGetLastError();
+      c->pdl = false;
+      e = launch_expert_fused(fa, c->plan, c->fused_grid, s, false);
+    }
+    prof_end(c, s, &pe);
+    if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("expert_fused launch: ") + cudaGetErrorString(e));
+    c->fused_calls += 1;
+  } else {
+    prof_begin(c, 1, s, &pe);
+    launch_expert_gateup(ea, s, c->num_sms);
+    prof_end(c, s, &pe);
+    prof_begin(c, 2, s, &pe);
+    launch_expert_down(ea, s, c->num_sms);
+    prof_end(c, s, &pe);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (c->P > 1) {
+    prof_begin(c, 3, s, &pe);
+    ncclResult_t r = g_nccl.AllReduce(y, y, (size_t)c->d, ncclFloat32, ncclSum, c->comm, s);
+    prof_end(c, s, &pe);
+    if (r != ncclSuccess) return fail(MOE_ERR_NCCL, "ncclAllReduce failed");
+  }
+  CUDA_TRY(cudaEventRecord(c->done_ev, s));
+  c->any_call = true;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_layer_forward(moe_ctx* c, int32_t layer, const void* x, float* y, void* stream) {
+  if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
+  DeviceGuard g(c->device);
+  return forward_impl(c, layer, x, y, (cudaStream_t)stream);
+}
+
+MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint16_t* x_host, float* y_host) {
+  if (!c || !x_host || !y_host) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
+  if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
+  DeviceGuard g(c->device);
+  cudaStream_t s = c->own_stream;
+  CUDA_TRY(cudaMemcpyAsync(c->d_x_e2e, x_host, sizeof(uint16_t) * c->d, cudaMemcpyHostToDevice, s));
+  moe_status st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s);
+  if (st != MOE_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(y_host, c->d_y_e2e, sizeof(float) * c->d, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return MOE_OK;
+}
+
+MOE_API moe_status cache_stats(moe_ctx* c, int32_t layer, moe_layer_stats* out) {
+  if (!c || !out) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
+  if (layer < -1 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
+  DeviceGuard g(c->device);
+  moe_status st = drain(c);
+  if (st != MOE_OK) return st;
+  std::vector<DevStats> all(c->L);
+  CUDA_TRY(cudaMemcpy(all.data(), c->d_stats, sizeof(DevStats) * c->L, cudaMemcpyDeviceToHost));
+  DevStats acc;
+  memset(&acc, 0, sizeof(acc));
+  for (int l = 0; l < c->L; ++l) {
+    if (layer >= 0 && l != layer) continue;
+    const unsigned long long* src = (const unsigned long long*)&all[l];
+    unsigned long long* dst = (unsigned long long*)&acc;
+    for (size_t k = 0; k < sizeof(DevStats) / 8; ++k) dst[k] += src[k];
+  }
+  memcpy(out, &acc, sizeof(acc));
+  return MOE_OK;
+}
+
+MOE_API moe_status cache_trace(moe_ctx* c, moe_access_record* host_out, int64_t cap, int64_t* n_out) {
+  if (!c || (cap > 0 && !host_out) || cap < 0) return fail(MOE_ERR_INVALID_ARG, "bad argument");
+  if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
+  DeviceGuard g(c->device);
+  moe_status st = drain(c);
+  if (st != MOE_OK) return st;
+  long long avail = c->trace_count < c->trace_cap ? c->trace_count : c->trace_cap;
+  long long m = avail < cap ? avail : cap;
+  if (m > 0)
+    CUDA_TRY(cudaMemcpy(host_out, c->d_trace, sizeof(moe_access_record) * m, cudaMemcpyDeviceToHost));
+  if (n_out) *n_out = c->trace_count;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_profile_enable(moe_ctx* c, int32_t enable) {
+  if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
+  c->prof = enable != 0;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_profile_read(moe_ctx* c, moe_profile_t* out) {
+  if (!c || !out) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  DeviceGuard g(c->device);
+  for (auto& p : c->prof_events) {
+    float ms = 0;
+    CUDA_TRY(cudaEventSynchronize(p.b));
+    CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+    c->prof_ms[p.kind] += ms;
+    c->prof_launches[p.kind] += 1;
+    c->ev_free.push_back(p.a);
+    c->ev_free.push_back(p.b);
+  }
+  c->prof_events.clear();
+  for (int k = 0; k < MOE_PROF_KINDS; ++k) {
+    out->ms[k] = c->prof_ms[k];
+    out->launches[k] = c->prof_launches[k];
+    c->prof_ms[k] = 0;
+    c->prof_launches[k] = 0;
+  }
+  return MOE_OK;
+}
+
+}  // extern "C"
