@@ -195,6 +195,15 @@ typedef struct {
 MOE_API moe_status moe_profile_enable(moe_ctx* ctx, int32_t enable);
 MOE_API moe_status moe_profile_read(moe_ctx* ctx, moe_profile_t* out);
 
+/* Which kernels this context launches (diagnostics): expert_path 1 = fused persistent
+ * expert kernel (bulk-copy ring, grid barrier), 0 = split gate/up + down kernels (used
+ * when the fused plan does not fit shared memory); pdl = programmatic dependent launch
+ * in use; ring_stages / stage_bytes / grid of the fused kernel. */
+typedef struct {
+  int32_t expert_path, pdl, ring_stages, stage_bytes, grid, reserved[3];
+} moe_runtime_info;
+MOE_API moe_status moe_get_runtime_info(moe_ctx* ctx, moe_runtime_info* out);
+
 /* 128-byte NCCL unique id for a TP group (dlopens libnccl.so.2). */
 MOE_API moe_status moe_nccl_unique_id(uint8_t* out128);
 

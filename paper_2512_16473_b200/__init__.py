@@ -153,6 +153,12 @@ class Moe:
         _check("cache_trace", lib().cache_trace(self._h, out.ctypes.data if m else None, m, ctypes.byref(n)))
         return out
 
+    def runtime_info(self) -> dict:
+        r = _abi.RuntimeInfo()
+        _check("moe_get_runtime_info", lib().moe_get_runtime_info(self._h, ctypes.byref(r)))
+        return {"expert_path": "fused" if r.expert_path else "split", "pdl": bool(r.pdl),
+                "ring_stages": r.ring_stages, "stage_bytes": r.stage_bytes, "grid": r.grid}
+
     def profile(self, enable: bool = True) -> None:
         _check("moe_profile_enable", lib().moe_profile_enable(self._h, int(enable)))
 

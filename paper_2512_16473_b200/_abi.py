@@ -21,7 +21,8 @@ POLICY_LRU, POLICY_FIFO, POLICY_STATIC_RANDOM = 0, 1, 2
 PROF_KINDS = ("route_probe", "expert_ffn", "expert_down", "allreduce")
 EXPORTS = ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward",
            "moe_layer_forward_host", "cache_stats", "cache_trace", "moe_profile_enable",
-           "moe_profile_read", "moe_nccl_unique_id", "moe_last_error", "moe_abi_version")
+           "moe_profile_read", "moe_nccl_unique_id", "moe_last_error", "moe_abi_version",
+           "moe_get_runtime_info")
 
 
 class ModelDesc(ctypes.Structure):
@@ -56,6 +57,11 @@ class LayerStats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint64) for f in STAT_FIELDS]
 
 
+class RuntimeInfo(ctypes.Structure):
+    _fields_ = [("expert_path", ctypes.c_int32), ("pdl", ctypes.c_int32), ("ring_stages", ctypes.c_int32),
+                ("stage_bytes", ctypes.c_int32), ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+
+
 class Profile(ctypes.Structure):
     _fields_ = [("ms", ctypes.c_double * 4), ("launches", ctypes.c_uint64 * 4)]
 
@@ -84,9 +90,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.moe_profile_enable.argtypes = [p, i32]
     lib.moe_profile_read.argtypes = [p, ctypes.POINTER(Profile)]
     lib.moe_nccl_unique_id.argtypes = [p]
+    lib.moe_get_runtime_info.argtypes = [p, ctypes.POINTER(RuntimeInfo)]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_abi_version.restype = i32
     for name in ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward", "moe_layer_forward_host",
-                 "cache_stats", "cache_trace", "moe_profile_enable", "moe_profile_read", "moe_nccl_unique_id"):
+                 "cache_stats", "cache_trace", "moe_profile_enable", "moe_profile_read", "moe_nccl_unique_id",
+                 "moe_get_runtime_info"):
         getattr(lib, name).restype = i32
     return lib

@@ -27,11 +27,13 @@ struct RouteRec {
   float w[kMaxK];
   int32_t slot[kMaxK];   // slot index in the pool (cache way or staging slot)
   uint32_t gen[kMaxK];   // fill generation the slot must reach before it is read
+  int32_t miss[kMaxK];   // 1: filled by this call -> wait for gen; 0: hit, already landed
 };
 
-// One mailbox entry per call, in HOST-MAPPED pinned memory. The router kernel writes the
-// payload, fences (system scope), then publishes `seq`; the runtime's fetch thread polls
-// `seq` and issues the copies of the missed experts on the fetch stream.
+// Miss mailbox entry, in HOST-MAPPED pinned memory, written by the router kernel only for
+// calls that missed: payload, system fence, then `seq`. Every call also publishes its seq
+// in a host-mapped progress word; the runtime's fetch thread scans seqs up to it and
+// issues the copies of the missed experts on the fetch stream.
 struct Mail {
   volatile unsigned long long seq;
   int32_t layer, nmiss;
@@ -57,8 +59,10 @@ struct RouteArgs {
   long long trace_idx, trace_cap;
   uint32_t token;
   Mail* mail;          // device alias of the host-mapped ring entry for this call
+  volatile unsigned long long* last_seq;  // device alias of the host-mapped progress word
   unsigned long long seq;
   long long slot_bytes;
+  float* y_zero;       // if non-null: zero y[0..d) (the fused expert kernel accumulates into it)
 };
 
 struct ExpertArgs {
@@ -76,17 +80,19 @@ struct ExpertArgs {
 constexpr int kFusedMaxDynSmem = 232448 - 1024;  // 227 KB opt-in minus static shared memory
 struct FusedArgs {
   ExpertArgs e;
-  unsigned long long* bar;        // grid-barrier counter (monotonic across calls)
-  unsigned long long bar_target;  // (call index + 1) * gridDim.x
+  unsigned long long* bar;        // per-expert group-barrier counters [K] (monotonic across calls)
+  unsigned long long calls;       // number of earlier fused launches on this context
   int NS, SB;                     // ring stages / stage bytes
   int xh_bytes, ypart_bytes;
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
+  unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_KERNEL=1) or nullptr
 };
 struct FusedPlan {
   int SB, NS, xh_bytes, ypart_bytes, threads;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int K, int grid, FusedPlan* p);
+
 cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl);
 cudaError_t preload_fused_kernels();
 

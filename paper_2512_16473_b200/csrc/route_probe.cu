@@ -66,6 +66,9 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
   }
   griddep_launch_dependents();  // let the expert kernel's CTAs get resident early
   griddep_wait();               // x and the previous calls' directory writes are visible now
+  if (a.y_zero)                 // the fused expert kernel accumulates the K experts into y
+    for (int i = threadIdx.x; i < (a.d >> 2); i += kThreads)
+      reinterpret_cast<float4*>(a.y_zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int4* xv = reinterpret_cast<const int4*>(a.x);
   float acc = 0.f;
   if (active) {
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
   int myHit = 0, myWay = -1, myEv = -1, mySlot = 0;
   uint32_t myGen = 0;
   unsigned long long clock = 0;
-  int nhit = 0, nev = 0, huf = 0;
+  int nhit = 0, nev = 0;
   if (a.covered) {
     int32_t tag = lane < M ? a.tag[lane] : -2;
     unsigned long long st = lane < M ? a.stamp[lane] : 0ull;
@@ -173,10 +176,6 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     if (lane < K) {
       mySlot = a.slot_base + myWay;
       myGen = g;
-      if (myHit) {
-        const uint32_t rd = *((volatile const uint32_t*)(a.ready + mySlot));
-        huf = rd < g;
-      }
     }
   } else {
     // beyond coverage: every expert is fetched into a staging slot, never inserted
@@ -188,7 +187,6 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
   }
   nhit = __popc(__ballot_sync(0xffffffffu, lane < K && myHit));
   nev = __popc(__ballot_sync(0xffffffffu, lane < K && myEv >= 0));
-  huf = __popc(__ballot_sync(0xffffffffu, lane < K && huf));
   const unsigned missmask = __ballot_sync(0xffffffffu, lane < K && !myHit);
 
   // ---- route record, trace, mailbox
@@ -197,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     a.route->w[lane] = sW[lane];
     a.route->slot[lane] = mySlot;
     a.route->gen[lane] = myGen;
+    a.route->miss[lane] = !myHit;
     if (a.trace_idx + lane < a.trace_cap) {
       moe_access_record rec;
       rec.token = a.token;
@@ -218,28 +217,42 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
       a.mail->gen[i] = myGen;
     }
   }
+  const int nmiss = K - nhit;
   if (lane == 0) {
     a.route->K = K;
     if (a.covered) *a.clock = clock;
+    // Counters: fire-and-forget reductions (RED), so the critical path never waits on
+    // the read-modify-write round trips.
     DevStats* s = a.stats;
-    const int nmiss = K - nhit;
-    s->accesses += 1;
-    s->at_least_one_hit += nhit > 0;
-    s->all_k_hit += nhit == K;
-    s->expert_hits += nhit;
-    s->expert_misses += nmiss;
-    s->coverage_misses += a.covered ? 0 : K;
-    s->evictions += nev;
-    s->fetches += nmiss;
-    s->fetch_bytes += (unsigned long long)nmiss * (unsigned long long)a.slot_bytes;
-    s->hit_under_fill += huf;
-    a.mail->layer = a.layer;
-    a.mail->nmiss = nmiss;
+    atomicAdd(&s->accesses, 1ull);
+    if (nhit > 0) atomicAdd(&s->at_least_one_hit, 1ull);
+    if (nhit == K) atomicAdd(&s->all_k_hit, 1ull);
+    if (nhit) atomicAdd(&s->expert_hits, (unsigned long long)nhit);
+    if (nmiss) {
+      atomicAdd(&s->expert_misses, (unsigned long long)nmiss);
+      atomicAdd(&s->fetches, (unsigned long long)nmiss);
+      atomicAdd(&s->fetch_bytes, (unsigned long long)nmiss * (unsigned long long)a.slot_bytes);
+    }
+    if (!a.covered) atomicAdd(&s->coverage_misses, (unsigned long long)K);
+    if (nev) atomicAdd(&s->evictions, (unsigned long long)nev);
+    // hit_under_fill stays 0 here: a miss is filled before this call's experts are read,
+    // so no later access can find the slot still filling.
+    if (nmiss) {
+      a.mail->layer = a.layer;
+      a.mail->nmiss = nmiss;
+    }
   }
   __syncwarp();
   if (lane == 0) {
-    __threadfence_system();
-    a.mail->seq = a.seq;  // publish (volatile store to host-mapped memory)
+    // Miss mailbox (host-mapped): an entry is written only when this call missed; the
+    // progress word last_seq is written on every call. A system fence orders the entry
+    // before both words, so last_seq >= seq implies entry(seq) is complete if it exists.
+    if (nmiss) {
+      __threadfence_system();
+      a.mail->seq = a.seq;
+      __threadfence_system();
+    }
+    *a.last_seq = a.seq;
   }
 }
 
@@ -248,6 +261,13 @@ __global__ void write_ready_kernel(uint32_t* ready, int slot, uint32_t gen) {
 }
 
 }  // namespace
+
+cudaError_t preload_route_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, route_probe_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, write_ready_kernel);
+  return e;
+}
 
 cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl) {
   cudaLaunchConfig_t cfg = {};
@@ -260,13 +280,6 @@ cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl) {
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, route_probe_kernel, a);
-}
-
-cudaError_t preload_route_kernels() {
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, route_probe_kernel);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, write_ready_kernel);
-  return e;
 }
 
 void launch_write_ready(uint32_t* ready, int slot, uint32_t gen, cudaStream_t s) {

@@ -118,6 +118,8 @@ struct moe_ctx {
   // mailbox + fetch thread
   Mail* h_mail = nullptr;
   Mail* d_mail = nullptr;
+  volatile unsigned long long* h_last = nullptr;  // host-mapped progress word
+  unsigned long long* d_last = nullptr;
   std::atomic<unsigned long long> issued{0}, consumed{0};
   std::atomic<bool> stop{false};
   std::atomic<int> fetch_error{0};
@@ -144,6 +146,7 @@ struct moe_ctx {
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
+  unsigned long long* d_ts = nullptr;  // per-CTA phase timestamps (MOE_DEBUG_KERNEL=1)
 };
 
 namespace {
@@ -166,26 +169,26 @@ void fetch_thread_main(moe_ctx* c) {
   const long delay_us = dly ? atol(dly) : 0;
   const bool log = getenv("MOE_DEBUG_FETCH_LOG") != nullptr;
   unsigned long long next = c->consumed.load() + 1;
-  auto idle_since = std::chrono::steady_clock::now();
+  std::chrono::steady_clock::time_point stop_seen{};
+  bool stopping = false;
   while (true) {
-    if (next > c->issued.load(std::memory_order_acquire)) {
-      if (c->stop.load()) break;
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    const unsigned long long last = *c->h_last;  // device progress (every call publishes)
+    if (next > last) {
+      if (c->stop.load()) {
+        if (next > c->issued.load()) break;
+        if (!stopping) { stopping = true; stop_seen = std::chrono::steady_clock::now(); }
+        // the device never published (e.g. a trapped kernel): give up after 5 s
+        if (std::chrono::steady_clock::now() - stop_seen > std::chrono::seconds(5)) break;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(next <= c->issued.load() ? 2 : 20));
       continue;
     }
     Mail* m = &c->h_mail[next % kMailRing];
-    int spins = 0;
-    idle_since = std::chrono::steady_clock::now();
-    bool abandoned = false;
-    while (m->seq != next) {
-      if (++spins > 2000) std::this_thread::sleep_for(std::chrono::microseconds(10));
-      if (c->stop.load() &&
-          std::chrono::steady_clock::now() - idle_since > std::chrono::seconds(5)) {
-        abandoned = true;
-        break;
-      }
+    if (m->seq != next) {  // no miss in this call
+      c->consumed.store(next, std::memory_order_release);
+      ++next;
+      continue;
     }
-    if (abandoned) break;
     std::atomic_thread_fence(std::memory_order_acquire);
     const int layer = m->layer, nmiss = m->nmiss;
     for (int i = 0; i < nmiss; ++i) {
@@ -289,6 +292,14 @@ extern "C" {
 MOE_API const char* moe_last_error(void) { return g_err.c_str(); }
 MOE_API int32_t moe_abi_version(void) { return MOE_ABI_VERSION; }
 
+// Debug only (not in moe.h): per-CTA timestamps of the last fused launch -> host (grid*8).
+MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
+  if (!c || !c->d_ts) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * 8 * c->fused_grid, cudaMemcpyDeviceToHost);
+  return c->fused_grid;
+}
+
 // Debug only (not in moe.h): host pointer to the mapped kernel progress words, or NULL.
 MOE_API const unsigned* moe_debug_words(moe_ctx* c) { return c ? c->h_dbg : nullptr; }
 
@@ -365,25 +376,38 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaHostAlloc((void**)&c->h_mail, sizeof(Mail) * kMailRing, cudaHostAllocMapped));
   memset((void*)c->h_mail, 0, sizeof(Mail) * kMailRing);
   INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_mail, c->h_mail, 0));
+  {
+    unsigned long long* hl = nullptr;
+    INIT_TRY(cudaHostAlloc((void**)&hl, 64, cudaHostAllocMapped));
+    memset(hl, 0, 64);
+    c->h_last = hl;
+    INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_last, hl, 0));
+  }
   INIT_TRY(cudaMalloc(&c->d_route, sizeof(RouteRec)));
   INIT_TRY(cudaMalloc(&c->d_h, sizeof(float) * (size_t)K * c->ffr));
   INIT_TRY(cudaMalloc(&c->d_x_e2e, sizeof(uint16_t) * d));
   INIT_TRY(cudaMalloc(&c->d_y_e2e, sizeof(float) * d));
-  INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long)));
-  INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long)));
+  INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * kMaxK));
+  INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * kMaxK));
   {
     const char* path = getenv("MOE_EXPERT_PATH");
     const char* pdl = getenv("MOE_PDL");
     c->pdl = !(pdl && pdl[0] == '0');
     c->fused_grid = c->num_sms;
     c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, K, c->fused_grid, &c->plan);
-    if (getenv("MOE_DEBUG_KERNEL")) {
+    if (getenv("MOE_DEBUG_KERNEL")) {  // progress words in host-mapped memory (slow: PCIe atomics)
       INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
       memset(c->h_dbg, 0, 64);
       INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_dbg, c->h_dbg, 0));
+    }
+    if (getenv("MOE_DEBUG_TS")) {      // per-CTA phase timestamps in device memory (cheap)
+      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 8 * c->fused_grid));
+      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 8 * c->fused_grid));
+    }
+    if (getenv("MOE_DEBUG_KERNEL") || getenv("MOE_DEBUG_TS")) {
       fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d xh=%d ypart=%d smem=%zu grid=%d\n", (int)c->fused,
               c->plan.NS, c->plan.SB, c->plan.xh_bytes, c->plan.ypart_bytes, c->plan.smem, c->fused_grid);
-    }
+  }
   }
   {
     void* fn = nullptr;
@@ -433,7 +457,9 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_x_e2e);
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_bar);
+  cudaFree(c->d_ts);
   if (c->h_mail) cudaFreeHost(c->h_mail);
+  if (c->h_last) cudaFreeHost((void*)c->h_last);
   for (void* p : c->registered) cudaHostUnregister(p);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
   if (c->fetch_stream) cudaStreamDestroy(c->fetch_stream);
@@ -568,6 +594,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.trace_cap = c->trace_cap;
   ra.token = c->tokens[layer];
   ra.mail = c->d_mail + (seq % kMailRing);
+  ra.last_seq = c->d_last;
+  ra.y_zero = (c->fused && c->K == 2) ? y : nullptr;  // the fused kernel reduces the K experts into y
   ra.seq = seq;
   ra.slot_bytes = c->slot_bytes;
 
@@ -592,12 +620,13 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     FusedArgs fa;
     fa.e = ea;
     fa.bar = c->d_bar;
-    fa.bar_target = (c->fused_calls + 1) * (unsigned long long)c->fused_grid;
+    fa.calls = c->fused_calls;
     fa.NS = c->plan.NS;
     fa.SB = c->plan.SB;
     fa.xh_bytes = c->plan.xh_bytes;
     fa.ypart_bytes = c->plan.ypart_bytes;
     fa.dbg = c->d_dbg;
+    fa.ts = c->d_ts;
     prof_begin(c, 1, s, &pe);
     cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl);
     if (e != cudaSuccess && c->pdl) {  // cooperative + PDL not accepted: retry without PDL
@@ -680,6 +709,17 @@ MOE_API moe_status cache_trace(moe_ctx* c, moe_access_record* host_out, int64_t 
   if (m > 0)
     CUDA_TRY(cudaMemcpy(host_out, c->d_trace, sizeof(moe_access_record) * m, cudaMemcpyDeviceToHost));
   if (n_out) *n_out = c->trace_count;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_get_runtime_info(moe_ctx* c, moe_runtime_info* out) {
+  if (!c || !out) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  memset(out, 0, sizeof(*out));
+  out->expert_path = c->fused ? 1 : 0;
+  out->pdl = c->pdl ? 1 : 0;
+  out->ring_stages = c->fused ? c->plan.NS : 0;
+  out->stage_bytes = c->fused ? c->plan.SB : 0;
+  out->grid = c->fused ? c->fused_grid : 0;
   return MOE_OK;
 }
 
