@@ -183,10 +183,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     nccl_id = None
     if world > 1:
         import torch.distributed as dist
+        from paper_2512_16473_b200 import tp
         dist.init_process_group("nccl", device_id=dev)
-        obj = [moe.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = tp.broadcast_nccl_id()
     hm = harness.host_model(1, CFG["d"], CFG["ff"], CFG["n"], CFG["K"], tp_size=world, tp_rank=rank)
     x, _ = harness.hidden_states(hm, TRACE_TOKENS, "paper")
     xd = torch.from_numpy(x.view(np.int16)).to(dev)          # [T][1][d] resident in HBM

@@ -58,8 +58,8 @@ def host_model(L: int, d: int, ff: int, n: int, K: int, tp_size: int = 1, tp_ran
     sb = moe.slot_bytes(d, ff, tp_size)
     total = L * n * sb
     if pinned and torch is not None:
-        buf = torch.empty(total, dtype=torch.uint8, pin_memory=True)
-        arr = buf.numpy()
+        buf = moe.PinnedBuffer(total)     # cudaHostAlloc, exact size (torch rounds to 2^k)
+        arr = buf.array
     else:
         buf = arr = np.empty(total, np.uint8)
         pinned = False

@@ -204,6 +204,11 @@ typedef struct {
 } moe_runtime_info;
 MOE_API moe_status moe_get_runtime_info(moe_ctx* ctx, moe_runtime_info* out);
 
+/* Page-locked host memory for the backing store (cudaHostAlloc, portable): exact size,
+ * no power-of-two rounding. Pass already_pinned = 1 in moe_weights for blobs inside it. */
+MOE_API moe_status moe_host_alloc(int64_t bytes, void** out);
+MOE_API moe_status moe_host_free(void* p);
+
 /* 128-byte NCCL unique id for a TP group (dlopens libnccl.so.2). */
 MOE_API moe_status moe_nccl_unique_id(uint8_t* out128);
 

@@ -15,7 +15,7 @@ from . import _abi
 from ._abi import (POLICY_FIFO, POLICY_LRU, POLICY_STATIC_RANDOM, PROF_KINDS, RECORD_DTYPE,
                    STAT_FIELDS)
 
-__all__ = ["Moe", "MoeError", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
+__all__ = ["Moe", "MoeError", "PinnedBuffer", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
            "STAT_FIELDS", "slot_bytes", "blob_views", "lib", "nccl_unique_id", "PROF_KINDS"]
 
 _lib = None
@@ -51,6 +51,29 @@ def blob_views(blob: np.ndarray, d: int, ffr: int):
     assert u16.size == 3 * d * ffr
     n = ffr * d
     return u16[:n].reshape(ffr, d), u16[n:2 * n].reshape(ffr, d), u16[2 * n:].reshape(d, ffr)
+
+
+class PinnedBuffer:
+    """Page-locked host buffer from moe_host_alloc (exact size), exposed as a numpy uint8 array."""
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _check("moe_host_alloc", lib().moe_host_alloc(nbytes, ctypes.byref(p)))
+        self._p = p
+        self.nbytes = nbytes
+        self.array = np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(p.value))
+
+    def free(self) -> None:
+        if getattr(self, "_p", None):
+            self.array = None
+            lib().moe_host_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def nccl_unique_id() -> bytes:

@@ -22,7 +22,7 @@ PROF_KINDS = ("route_probe", "expert_ffn", "expert_down", "allreduce")
 EXPORTS = ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward",
            "moe_layer_forward_host", "cache_stats", "cache_trace", "moe_profile_enable",
            "moe_profile_read", "moe_nccl_unique_id", "moe_last_error", "moe_abi_version",
-           "moe_get_runtime_info")
+           "moe_get_runtime_info", "moe_host_alloc", "moe_host_free")
 
 
 class ModelDesc(ctypes.Structure):
@@ -91,10 +91,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.moe_profile_read.argtypes = [p, ctypes.POINTER(Profile)]
     lib.moe_nccl_unique_id.argtypes = [p]
     lib.moe_get_runtime_info.argtypes = [p, ctypes.POINTER(RuntimeInfo)]
+    lib.moe_host_alloc.argtypes = [i64, ctypes.POINTER(p)]
+    lib.moe_host_free.argtypes = [p]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_abi_version.restype = i32
     for name in ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward", "moe_layer_forward_host",
                  "cache_stats", "cache_trace", "moe_profile_enable", "moe_profile_read", "moe_nccl_unique_id",
-                 "moe_get_runtime_info"):
+                 "moe_get_runtime_info", "moe_host_alloc", "moe_host_free"):
         getattr(lib, name).restype = i32
     return lib

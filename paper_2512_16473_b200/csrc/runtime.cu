@@ -303,6 +303,24 @@ MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
 // Debug only (not in moe.h): host pointer to the mapped kernel progress words, or NULL.
 MOE_API const unsigned* moe_debug_words(moe_ctx* c) { return c ? c->h_dbg : nullptr; }
 
+MOE_API moe_status moe_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes <= 0) return fail(MOE_ERR_INVALID_ARG, "bad argument");
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return fail(MOE_ERR_OUT_OF_MEMORY, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  }
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_host_free(void* p) {
+  if (!p) return MOE_OK;
+  CUDA_TRY(cudaFreeHost(p));
+  return MOE_OK;
+}
+
 MOE_API moe_status moe_nccl_unique_id(uint8_t* out128) {
   if (!out128) return fail(MOE_ERR_INVALID_ARG, "out128 is NULL");
   std::string why;

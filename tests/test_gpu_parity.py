@@ -228,3 +228,79 @@ def test_phi_shape_miss_fetch_two_layers():
         m.configure(ways=4, indexes=1)
         y = harness.run_decode(m, x)
         _compare(hm, m, x, ref, y)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_tp_ff_split_emulated_on_one_gpu(P):
+    """north_star (4) on one GPU: each rank's ff slice is itself a valid tp_size=1 model
+    with d_ff = ff/P; run the P slices sequentially, sum the partial y (what the per-layer
+    NCCL all-reduce does) and compare with the unsplit oracle. Routing / cache traces
+    must be identical on every rank."""
+    L, d, ff, n, K, T = 2, 256, 1024, 8, 2, 6
+    full = harness.host_model(L, d, ff, n, K)
+    x, _ = harness.hidden_states(full, T, "paper")
+    ref = _oracle_run(full, x, N=L, M=2)
+    ys, traces = [], []
+    for p in range(P):
+        hp = harness.host_model(L, d, ff, n, K, tp_size=P, tp_rank=p)
+        with moe.Moe(L, d, ff // P, n, K, hp.gates, hp.blobs, already_pinned=hp.pinned) as m:
+            m.configure(ways=2, indexes=L)
+            ys.append(harness.run_decode(m, x))
+            traces.append(m.trace())
+    for tr in traces:
+        for f in EXACT_FIELDS:
+            np.testing.assert_array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    y = np.sum(np.stack(ys).astype(np.float64), axis=0)
+    for t in range(T):
+        for l in range(L):
+            r = ref.y[t, l]
+            assert np.abs(y[t, l] - r).max() / np.abs(r).max() <= TIGHT
+
+
+def _tp_nccl_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    from paper_2512_16473_b200 import tp
+    nid = tp.broadcast_nccl_id()
+    L, d, ff, n, K, T = 2, 256, 1024, 8, 2, 5
+    hm = harness.host_model(L, d, ff, n, K, tp_size=world, tp_rank=rank)
+    x, _ = harness.hidden_states(hm, T, "paper")
+    with harness.open_moe(hm, device=rank, nccl_id=nid) as m:
+        m.configure(ways=2, indexes=L)
+        y = harness.run_decode(m, x, device=rank)
+        tr = m.trace()
+    if rank == 0:
+        full = harness.host_model(L, d, ff, n, K)
+        ref = _oracle_run(full, x, N=L, M=2)
+        err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
+                  for t in range(T) for l in range(L))
+        same = all(np.array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64)) for f in EXACT_FIELDS)
+        q.put((err, same))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_tp2_nccl_allreduce_multi_gpu():
+    """Real ff-split over 2 GPUs with the library's NCCL all-reduce (skipped on 1 GPU)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err, same = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert same and err <= TIGHT
