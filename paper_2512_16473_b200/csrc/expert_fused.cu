@@ -8,9 +8,10 @@
 // tensor-core contraction. Design for B200:
 //  - one CTA per SM (grid = #SMs, cooperative => co-resident). The CTAs are split into K
 //    groups, group r serving routed expert r only: its phase A rows j and its phase B
-//    rows c, in balanced contiguous ranges. The barrier between the phases is therefore
-//    per expert (the CTAs that produce h_r), and a CTA needs only ONE expert's h in
-//    shared memory, which leaves room for a large weight ring;
+//    rows c — 88% in static contiguous blocks, the tail claimed in small chunks from a
+//    per-expert counter (per-SM HBM bandwidth varies by ~10%; stealing evens it out). The
+//    barrier between the phases is per expert (the CTAs that produce h_r), and a CTA needs
+//    only ONE expert's h in shared memory, which leaves room for a large weight ring;
 //  - warp 0 / lane 0 is a producer streaming weight rows with bulk async copies
 //    (cp.async.bulk — the TMA engine's linear path, SASS UBLKCP) into an NS-stage shared
 //    memory ring guarded by full/empty mbarriers (L2 evict-first). Bytes in flight per SM
@@ -32,31 +33,30 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kMaxNC = 16;              // consumer warps (one per ring stage; NS <= kMaxNC)
-constexpr int kThreadsF = 32 * (kMaxNC + 1);
+constexpr int kMaxNS = 10;                 // ring stages (phase B pairs them: NS even)
+constexpr int kWarpsPerStage = 2;          // consumer warps sharing one stage
+constexpr int kThreadsF = 32 * (1 + kWarpsPerStage * kMaxNS);
 
-__device__ __forceinline__ float dot8_bb(const int4 w, const int4 x, float s) {
-  s = fmaf(bf_lo(w.x), bf_lo(x.x), s);
-  s = fmaf(bf_hi(w.x), bf_hi(x.x), s);
-  s = fmaf(bf_lo(w.y), bf_lo(x.y), s);
-  s = fmaf(bf_hi(w.y), bf_hi(x.y), s);
-  s = fmaf(bf_lo(w.z), bf_lo(x.z), s);
-  s = fmaf(bf_hi(w.z), bf_hi(x.z), s);
-  s = fmaf(bf_lo(w.w), bf_lo(x.w), s);
-  s = fmaf(bf_hi(w.w), bf_hi(x.w), s);
-  return s;
+// Packed fp32 FMA (sm_100: FFMA2): acc.{x,y} += a.{x,y} * b.{x,y}
+__device__ __forceinline__ float2 ffma2(const float2 a, const float2 b, const float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
 }
 
-__device__ __forceinline__ float dot8_bf(const int4 w, const float4 a, const float4 b, float s) {
-  s = fmaf(bf_lo(w.x), a.x, s);
-  s = fmaf(bf_hi(w.x), a.y, s);
-  s = fmaf(bf_lo(w.y), a.z, s);
-  s = fmaf(bf_hi(w.y), a.w, s);
-  s = fmaf(bf_lo(w.z), b.x, s);
-  s = fmaf(bf_hi(w.z), b.y, s);
-  s = fmaf(bf_lo(w.w), b.z, s);
-  s = fmaf(bf_hi(w.w), b.w, s);
-  return s;
+// bf16 pair (one 32-bit word) -> (lo, hi) fp32, exact
+__device__ __forceinline__ float2 bf2(uint32_t v) { return make_float2(bf_lo(v), bf_hi(v)); }
+
+// acc += w(8 bf16) . x(8 fp32)
+__device__ __forceinline__ float2 dot8(const int4 w, const float4 a, const float4 b, float2 acc) {
+  acc = ffma2(bf2(w.x), make_float2(a.x, a.y), acc);
+  acc = ffma2(bf2(w.y), make_float2(a.z, a.w), acc);
+  acc = ffma2(bf2(w.z), make_float2(b.x, b.y), acc);
+  acc = ffma2(bf2(w.w), make_float2(b.z, b.w), acc);
+  return acc;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -79,8 +79,38 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Shared-memory plan (bytes):  ring[NS][SB] | xh | ypart | full[NS] empty[NS] hbar
-//   xh = x (bf16) in phase A, then this group's h_r (fp32, 2-plane layout) in phase B.
+constexpr int kChunkA = 2;     // phase A rows per tail claim
+constexpr int kChunkB = 1;     // phase B rows per tail claim
+constexpr int kStaticPct = 88; // share of each phase's rows assigned statically (no atomics)
+
+// Static-then-steal schedule over `total` rows for CTA li of a group of gsz CTAs: the first
+// kStaticPct% of the rows are split into equal contiguous blocks, the tail is claimed in
+// chunks from a per-expert counter, so every CTA of the group ends each phase within about
+// one chunk of the others, whatever its share of HBM bandwidth.
+struct RowSched {
+  int s0, s1;    // this CTA's static block
+  int tail0;     // first tail row
+};
+__device__ __forceinline__ RowSched make_sched(int total, int li, int gsz) {
+  RowSched rs;
+  const int sb = (int)((long long)total * kStaticPct / 100 / gsz);
+  rs.s0 = li * sb;
+  rs.s1 = rs.s0 + sb;
+  rs.tail0 = gsz * sb;
+  return rs;
+}
+
+// Shared memory: ring[NS][SB] | xh | full[NS] empty[NS] hbar | meta[NS] | part[NS][2] |
+//                parB[NS/2]
+//  - phase A: stage s (16 KB) = one W1 row + one W3 row, consumed by warps 2s, 2s+1 (one
+//    half of the row each); x lives in xh as fp32.
+//  - phase B: stages (2u, 2u+1) form one super-stage holding a whole W2 row (<= 2*SB),
+//    guarded by full[2u]/empty[2u] and consumed by the 4 warps of stages 2u, 2u+1 (a
+//    quarter of the row each); h_r lives in xh as fp32 in the 2-plane layout.
+//  - partial sums of a stage's warps are combined in a fixed order after a named barrier
+//    (deterministic, no atomics). Every consumer warp waits on one mbarrier per phase, and
+//    its next wait is always one phase ahead of the part it just released: parity waits
+//    cannot alias.
 __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedArgs f) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ const uint8_t* sbase;
@@ -88,31 +118,34 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ int smiss, sslot;
   __shared__ uint32_t sgen;
   const ExpertArgs& a = f.e;
-  const int NS = f.NS, SB = f.SB;
+  const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
   uint8_t* ring = smem;
   uint8_t* xh = smem + (size_t)NS * SB;
-  float* ypart = reinterpret_cast<float*>(xh + f.xh_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ypart) + f.ypart_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(xh + f.xh_bytes);
   uint64_t* empty = full + NS;
   uint64_t* hbar = empty + NS;
+  volatile int* meta = reinterpret_cast<volatile int*>(hbar + 1);
+  volatile float* part = reinterpret_cast<volatile float*>(meta + NS);   // [NS][4]
+  volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 4 * NS);  // full[2u] parity at phase B start
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, d = a.d, ffr = a.ffr;
   const int G = gridDim.x, b = blockIdx.x;
-  // expert group of this CTA and its balanced ranges
+  // expert group of this CTA: group r serves routed expert r (phase A rows j and phase B
+  // rows c of that expert)
   const int r = (int)((long long)b * K / G);
-  const int gb0 = (int)(((long long)r * G + K - 1) / K);        // first CTA of group r
-  const int gb1 = (int)(((long long)(r + 1) * G + K - 1) / K);  // one past the last
+  const int gb0 = (int)(((long long)r * G + K - 1) / K);
+  const int gb1 = (int)(((long long)(r + 1) * G + K - 1) / K);
   const int gsz = gb1 - gb0, li = b - gb0;
-  const int ja = (int)((long long)ffr * li / gsz), jb = (int)((long long)ffr * (li + 1) / gsz);
-  const int nA = jb - ja;                       // phase A rows of expert r
-  const int c0 = (int)((long long)d * li / gsz), c1 = (int)((long long)d * (li + 1) / gsz);
-  const int nB = c1 - c0;                       // phase B rows of expert r
-  const int rowB = ffr * 2;                     // bytes of one W2 row
-  const int npB = (rowB + SB - 1) / SB;         // ring parts per phase B row
+  const int rowA = 4 * d;                       // bytes of one W1 row + one W3 row
+  const int rowB = ffr * 2;                     // bytes of one W2 row (<= 2*SB)
   const long long w2off = 2ll * ffr * d * 2;    // W2 offset in a slot
 
-  if (f.ts && threadIdx.x == 0) f.ts[b * 8 + 0] = globaltimer();
+  if (f.ts && threadIdx.x == 0) {
+    f.ts[b * 8 + 0] = globaltimer();
+    f.ts[b * 8 + 6] = 0;
+    f.ts[b * 8 + 7] = 0;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
@@ -121,7 +154,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(hbar, 1);
     fence_mbar_init();
   }
-  griddep_wait();  // route record / zeroed y (router kernel) and x (caller) are visible now
+  griddep_wait();  // route record / zeroed y and counters (router kernel), x (caller) visible
   if (f.ts && threadIdx.x == 0) f.ts[b * 8 + 1] = globaltimer();
   if (threadIdx.x == 0) {
     const int slot = a.route->slot[r];
@@ -131,8 +164,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     sbase = a.pool + (long long)slot * a.slot_bytes;
     swgt = a.route->w[r];
   }
-  for (int i = threadIdx.x; i < (d >> 3); i += kThreadsF)
-    reinterpret_cast<int4*>(xh)[i] = reinterpret_cast<const int4*>(a.x)[i];
+  for (int i = threadIdx.x; i < (d >> 2); i += kThreadsF) {  // x -> fp32 in shared memory
+    const uint2 v = reinterpret_cast<const uint2*>(a.x)[i];
+    reinterpret_cast<float4*>(xh)[i] = make_float4(bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y));
+  }
   __syncthreads();
   const uint8_t* base = sbase;
 
@@ -141,78 +176,144 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       if (smiss) wait_ready(a.ready, sslot, sgen);  // a hit's fill landed in an earlier call
+      unsigned* ctrA = f.ctr + r;
+      unsigned* ctrB = f.ctr + kMaxK + r;
+      uint32_t use = 0;                               // per-stage use-count parity bits
+      auto acquire = [&](int s) {                     // wait until stage s is free
+        mbar_wait(empty + s, ((use >> s) & 1) ^ 1);
+        use ^= 1u << s;
+      };
       int t = 0;
-      for (int j = ja; j < jb; ++j, ++t) {
+      auto issue_a = [&](int j) {
         const int s = t % NS;
-        mbar_wait(empty + s, ((t / NS) & 1) ^ 1);
+        acquire(s);
         const uint8_t* w1 = base + (long long)j * d * 2;
         const uint8_t* w3 = w1 + (long long)ffr * d * 2;
-        mbar_arrive_expect_tx(full + s, 4u * d);
+        meta[s] = j;
+        mbar_arrive_expect_tx(full + s, (uint32_t)rowA);
         bulk_g2s(ring + (size_t)s * SB, w1, 2u * d, full + s, pol);
         bulk_g2s(ring + (size_t)s * SB + 2 * d, w3, 2u * d, full + s, pol);
+        ++t;
+      };
+      // phase A: static block, then tail claims (two claims in flight hide the atomic latency)
+      const RowSched sa = make_sched(ffr, li, gsz);
+      unsigned c1 = atomicAdd(ctrA, (unsigned)kChunkA);
+      for (int j = sa.s0; j < sa.s1; ++j) issue_a(j);
+      unsigned c2 = atomicAdd(ctrA, (unsigned)kChunkA);
+      while (sa.tail0 + (int)c1 < ffr) {
+        const int j0 = sa.tail0 + (int)c1, j1 = min(j0 + kChunkA, ffr);
+        c1 = c2;
+        if (sa.tail0 + (int)c1 < ffr) c2 = atomicAdd(ctrA, (unsigned)kChunkA);
+        for (int j = j0; j < j1; ++j) issue_a(j);
       }
-      for (int i = 0; i < nB; ++i) {  // W2 rows do not depend on h: stream through the barrier
-        const uint8_t* row = base + w2off + (long long)(c0 + i) * rowB;
-        for (int p = 0; p < npB; ++p, ++t) {
-          const int s = t % NS;
-          const uint32_t bytes = (uint32_t)min(SB, rowB - p * SB);
-          mbar_wait(empty + s, ((t / NS) & 1) ^ 1);
-          mbar_arrive_expect_tx(full + s, bytes);
-          bulk_g2s(ring + (size_t)s * SB, row + (long long)p * SB, bytes, full + s, pol);
-        }
+      for (int k = 0; k < NS; ++k, ++t) {  // one end-of-phase marker per stage
+        const int s = t % NS;
+        acquire(s);
+        meta[s] = -1;
+        mbar_arrive(full + s);
       }
+      // phase B: whole W2 rows into super-stages (2u, 2u+1); W2 does not depend on h, so
+      // these loads stream while the consumers finish phase A and cross the barrier
+      int tb = 0;
+      auto issue_b = [&](int c) {
+        const int u = tb % NSB, s = 2 * u;
+        acquire(s);
+        meta[s] = c;
+        mbar_arrive_expect_tx(full + s, (uint32_t)rowB);
+        bulk_g2s(ring + (size_t)s * SB, base + w2off + (long long)c * rowB, (uint32_t)rowB, full + s, pol);
+        ++tb;
+      };
+      const RowSched sbk = make_sched(d, li, gsz);
+      c1 = atomicAdd(ctrB, (unsigned)kChunkB);
+      for (int c = sbk.s0; c < sbk.s1; ++c) issue_b(c);
+      c2 = atomicAdd(ctrB, (unsigned)kChunkB);
+      while (sbk.tail0 + (int)c1 < d) {
+        const int r0 = sbk.tail0 + (int)c1, r1 = min(r0 + kChunkB, d);
+        c1 = c2;
+        if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(ctrB, (unsigned)kChunkB);
+        for (int c = r0; c < r1; ++c) issue_b(c);
+      }
+      for (int k = 0; k < NSB; ++k, ++tb) {
+        const int s = 2 * (tb % NSB);
+        acquire(s);
+        meta[s] = -1;
+        mbar_arrive(full + s);
+      }
+      // publish the call's progress to the host fetch thread (PCIe write overlaps the tail)
+      if (b == 0) *a.last_seq = a.seq;
     }
     return;
   }
 
   // -------------------------------------------------------------------- consumers
-  // Ring part t (phase A row t, then phase B part t - nA) lives in stage t % NS and is
-  // consumed by warp t % NS: each consumer warp owns one stage, so its next wait is always
-  // exactly one mbarrier phase ahead of the part it just released (parity waits cannot
-  // alias) and the producer refills a stage as soon as its owner is done with it.
-  const int cw = warp - 1;
-  if (cw >= NS) return;
-  const int nthr = NS * 32;
+  const int cw = warp - 1;                 // consumer warp 0 .. 2*NS-1
+  if (cw >= kWarpsPerStage * NS) return;
+  const int nthr = kWarpsPerStage * NS * 32;
+  const int sA = cw >> 1, half = cw & 1;   // phase A: stage and half of the row
   float* hglob = a.h + (long long)r * ffr;
+  uint32_t ph = 0;                         // parity of the barrier this warp waits on
   {
-    const int nchA = d >> 3;
-    const int4* xv = reinterpret_cast<const int4*>(xh);
-    const int4* w1 = reinterpret_cast<const int4*>(ring + (size_t)cw * SB);
-    const int4* w3 = reinterpret_cast<const int4*>(ring + (size_t)cw * SB + 2 * d);
-    for (int t = cw; t < nA; t += NS) {
-      mbar_wait(full + cw, (t / NS) & 1);
-      if (f.ts && t == 0 && lane == 0) f.ts[b * 8 + 2] = globaltimer();
-      float g0 = 0.f, g1 = 0.f, u0 = 0.f, u1 = 0.f;
-#pragma unroll 2
-      for (int c = lane; c < nchA; c += 64) {
-        const int4 xa = xv[c];
-        g0 = dot8_bb(w1[c], xa, g0);
-        u0 = dot8_bb(w3[c], xa, u0);
-        if (c + 32 < nchA) {
-          const int4 xb = xv[c + 32];
-          g1 = dot8_bb(w1[c + 32], xb, g1);
-          u1 = dot8_bb(w3[c + 32], xb, u1);
-        }
+    const int nchA = d >> 3;               // 16-B chunks per W1 (or W3) row
+    const int c0 = half * (nchA >> 1), c1 = half ? nchA : (nchA >> 1);
+    const float4* xv = reinterpret_cast<const float4*>(xh);
+    const int4* w1 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB);
+    const int4* w3 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB + 2 * d);
+    bool first = true;
+    while (true) {
+      mbar_wait(full + sA, ph);
+      ph ^= 1;
+      const int j = meta[sA];
+      if (j < 0) break;
+      if (f.ts && first && cw == 0 && lane == 0) f.ts[b * 8 + 2] = globaltimer();
+      first = false;
+      const unsigned long long tp0 = (f.ts && cw == 0) ? globaltimer() : 0ull;
+      float2 g = make_float2(0.f, 0.f), u = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int c = c0 + lane; c < c1; c += 32) {
+        const float4 xa = xv[2 * c], xb = xv[2 * c + 1];
+        g = dot8(w1[c], xa, xb, g);
+        u = dot8(w3[c], xa, xb, u);
       }
-      const float g = warp_sum(g0 + g1);
-      const float u = warp_sum(u0 + u1);
-      __syncwarp();
+      const float gs = warp_sum(g.x + g.y);
+      const float us = warp_sum(u.x + u.y);
       if (lane == 0) {
-        mbar_arrive(empty + cw);
-        hglob[h_plane_index(ja + t, ffr)] = g / (1.0f + expf(-g)) * u;
+        part[4 * sA + 2 * half] = gs;
+        part[4 * sA + 2 * half + 1] = us;
+      }
+      named_bar_sync(2 + sA, 64);          // both halves of stage sA done (reads + partials)
+      if (half == 0 && lane == 0) {
+        mbar_arrive(empty + sA);
+        const float gg = part[4 * sA + 0] + part[4 * sA + 2];   // fixed order: half 0 + half 1
+        const float uu = part[4 * sA + 1] + part[4 * sA + 3];
+        hglob[h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
+        if (f.ts && cw == 0) f.ts[b * 8 + 6] += globaltimer() - tp0;
       }
     }
+    named_bar_sync(2 + sA, 64);
+    if (half == 0 && lane == 0) mbar_arrive(empty + sA);  // release the end marker's stage
+    if (half == 0 && lane == 0 && (sA & 1) == 0) parB[sA >> 1] = ph;  // full[sA] parity for phase B
   }
   named_bar_sync(1, nthr);
   if (f.ts && cw == 0 && lane == 0) f.ts[b * 8 + 3] = globaltimer();
+  if (f.ts && cw == 0 && lane == 0) f.ts[b * 8 + 7] = 0;
   // Per-expert barrier: all h_r rows (written by the gsz CTAs of this group) are visible
   // before any of them is read. Release-RED arrival, acquire spin (PTX memory model:
   // bar.sync + release at gpu scope publishes the whole CTA's writes).
   if (cw == 0 && lane == 0) {
-    unsigned long long* bar = f.bar + r;
+    unsigned long long* bar = f.bar + 16 * r;   // one 128-B line per expert group
     const unsigned long long target = (f.calls + 1) * (unsigned long long)gsz;
-    red_release_add_u64(bar, 1ull);
-    while (ld_acquire_u64(bar) < target) {
+    if (f.barmode == 1) {          // experiment: fence + relaxed atomic, relaxed spin + fence
+      __threadfence();
+      atomicAdd(bar, 1ull);
+      while (*((volatile unsigned long long*)bar) < target) __nanosleep(40);
+      __threadfence();
+    } else if (f.barmode == 2) {   // experiment: release RED, acquire spin without backoff
+      red_release_add_u64(bar, 1ull);
+      while (ld_acquire_u64(bar) < target) {
+      }
+    } else {
+      red_release_add_u64(bar, 1ull);
+      while (ld_acquire_u64(bar) < target) __nanosleep(40);
     }
     if (f.ts) f.ts[b * 8 + 4] = globaltimer();
     // h_r -> shared memory with one bulk copy (the async proxy reads global memory written
@@ -222,42 +323,41 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     bulk_g2s(xh, hglob, (uint32_t)ffr * 4u, hbar, policy_evict_first());
   }
   mbar_wait(hbar, 0);
-  const float4* hp0 = reinterpret_cast<const float4*>(xh);   // h[8c .. 8c+3]
-  const float4* hp1 = hp0 + (ffr >> 3);                      // h[8c+4 .. 8c+7]
   {
-    const int4* wv = reinterpret_cast<const int4*>(ring + (size_t)cw * SB);
-    const int totB = nB * npB;
-    int t = nA + ((cw - nA % NS) % NS + NS) % NS;  // first t >= nA with t % NS == cw
-    for (; t < nA + totB; t += NS) {
-      const int k = t - nA;
-      const int p = k % npB;
-      const int nck = min(SB, rowB - p * SB) >> 4;
-      const int cb = (p * SB) >> 4;
-      mbar_wait(full + cw, (t / NS) & 1);
-      float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll 2
-      for (int cc = lane; cc < nck; cc += 64) {
-        acc0 = dot8_bf(wv[cc], hp0[cb + cc], hp1[cb + cc], acc0);
-        if (cc + 32 < nck) acc1 = dot8_bf(wv[cc + 32], hp0[cb + cc + 32], hp1[cb + cc + 32], acc1);
+    const int u = cw >> 2, q = cw & 3;     // super-stage and quarter of the W2 row
+    if (u >= NSB) return;                  // (NS odd: the last stage's warps sit out phase B)
+    const int s = 2 * u;
+    ph = parB[u];
+    const int nck = rowB >> 4;
+    const int k0 = (nck * q) >> 2, k1 = (nck * (q + 1)) >> 2;
+    const float4* hp0 = reinterpret_cast<const float4*>(xh);   // h[8c .. 8c+3]
+    const float4* hp1 = hp0 + (ffr >> 3);                      // h[8c+4 .. 8c+7]
+    const int4* wv = reinterpret_cast<const int4*>(ring + (size_t)s * SB);
+    const float w = swgt;
+    while (true) {
+      mbar_wait(full + s, ph);
+      ph ^= 1;
+      const int c = meta[s];
+      if (c < 0) break;
+      const unsigned long long tp0 = (f.ts && cw == 0) ? globaltimer() : 0ull;
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int cc = k0 + lane; cc < k1; cc += 32) acc = dot8(wv[cc], hp0[cc], hp1[cc], acc);
+      const float sum = warp_sum(acc.x + acc.y);
+      if (lane == 0) part[4 * u + q] = sum;
+      named_bar_sync(2 + u, 128);          // the 4 quarters of this row are done
+      if (q == 0 && lane == 0) {
+        mbar_arrive(empty + s);
+        const float o = ((part[4 * u] + part[4 * u + 1]) + part[4 * u + 2]) + part[4 * u + 3];
+        if (K == 1) a.y[c] = w * o;
+        else red_add_f32(a.y + c, w * o);  // K == 2: 0 + a + b is order-independent
+        if (f.ts && cw == 0) f.ts[b * 8 + 7] += globaltimer() - tp0;
       }
-      const float acc = warp_sum(acc0 + acc1);
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(empty + cw);
-        ypart[k] = acc;
-      }
+      named_bar_sync(2 + u, 128);          // partials consumed before they are overwritten
     }
   }
-  named_bar_sync(1, nthr);
   if (f.ts && cw == 0 && lane == 0) f.ts[b * 8 + 5] = globaltimer();
   griddep_launch_dependents();
-  const float w = swgt;
-  for (int i = cw * 32 + lane; i < nB; i += nthr) {
-    float o = 0.f;
-    for (int p = 0; p < npB; ++p) o += ypart[i * npB + p];
-    if (K == 1) a.y[c0 + i] = w * o;
-    else red_add_f32(a.y + c0 + i, w * o);  // K == 2: 0 + a + b is order-independent
-  }
 }
 
 }  // namespace
@@ -272,22 +372,22 @@ cudaError_t preload_fused_kernels() {
 
 bool plan_fused(int d, int ffr, int K, int grid, FusedPlan* p) {
   if (K > 2 || grid < K) return false;          // deterministic combine needs K <= 2
-  const int SB = max(16384, 4 * d);
-  const int xh = ((max(2 * d, ffr * 4) + 127) / 128) * 128;   // x (bf16) | one expert's h (fp32)
-  const int gmin = grid / K;                                  // smallest group
-  const int cmax = (d + gmin - 1) / gmin + 1;
-  const int npB = (ffr * 2 + SB - 1) / SB;
-  const int ypart = ((cmax * npB * 4 + 15) / 16) * 16;
-  const int fixed = xh + ypart + 16;
-  int NS = (kFusedMaxDynSmem - fixed) / (SB + 16);
-  if (NS > kMaxNC) NS = kMaxNC;  // one consumer warp per stage
-  if (NS < 3) return false;
+  const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
+  if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
+  const int xh = ((max(4 * d, ffr * 4) + 127) / 128) * 128;   // x (fp32) | one expert's h (fp32)
+  const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + 64;
+  int NS = (kFusedMaxDynSmem - xh - tail) / SB;
+  if (NS > kMaxNS) NS = kMaxNS;
+  NS &= ~1;                                      // stages pair into super-stages in phase B
+  if (NS < 4) return false;
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;
-  p->ypart_bytes = ypart;
-  p->smem = (size_t)NS * SB + xh + ypart + 2 * NS * 8 + 8;
+  p->ypart_bytes = 0;
+  p->smem = (size_t)NS * SB + xh + tail;
   p->threads = kThreadsF;
+  p->partB = 2 * ffr;
+  p->copiesB = 1;
   return p->smem <= (size_t)kFusedMaxDynSmem;
 }
 

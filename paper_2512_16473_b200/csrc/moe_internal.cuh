@@ -59,10 +59,10 @@ struct RouteArgs {
   long long trace_idx, trace_cap;
   uint32_t token;
   Mail* mail;          // device alias of the host-mapped ring entry for this call
-  volatile unsigned long long* last_seq;  // device alias of the host-mapped progress word
   unsigned long long seq;
   long long slot_bytes;
   float* y_zero;       // if non-null: zero y[0..d) (the fused expert kernel accumulates into it)
+  unsigned* sched_zero;  // if non-null: zero the fused kernel's 2*kMaxK work-claim counters
 };
 
 struct ExpertArgs {
@@ -74,6 +74,8 @@ struct ExpertArgs {
   float* h;           // [K][ffr] SwiGLU activations (scratch)
   float* y;           // [d]
   const uint32_t* ready;
+  volatile unsigned long long* last_seq;  // host-mapped progress word, written at the end
+  unsigned long long seq;                 // this call's sequence number
 };
 
 // Fused persistent expert kernel (expert_fused.cu).
@@ -82,13 +84,17 @@ struct FusedArgs {
   ExpertArgs e;
   unsigned long long* bar;        // per-expert group-barrier counters [K] (monotonic across calls)
   unsigned long long calls;       // number of earlier fused launches on this context
+  unsigned* ctr;                  // work-claim counters [2][kMaxK] (phase A rows, phase B rows), zeroed per call
   int NS, SB;                     // ring stages / stage bytes
   int xh_bytes, ypart_bytes;
+  int partB;                      // bytes per W2-row part (<= SB, multiple of 16)
+  int copiesB;                    // bulk copies per phase B part (1 or 2)
+  int barmode;                    // phase barrier variant (experiments; 0 = default)
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_KERNEL=1) or nullptr
 };
 struct FusedPlan {
-  int SB, NS, xh_bytes, ypart_bytes, threads;
+  int SB, NS, xh_bytes, ypart_bytes, threads, partB, copiesB;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int K, int grid, FusedPlan* p);

@@ -64,8 +64,27 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     const int c = c0 + k * stride;
     if (active && c < nchunk) wv[k] = __ldg(wr + c);
   }
+  // The set of this layer was last written by the router kernel of an EARLIER call, which
+  // completed before the previous expert kernel passed its own griddepcontrol.wait, i.e.
+  // before this grid could launch: it can be read before this grid's wait, too.
+  int32_t dtag = -2;
+  unsigned long long dstamp = 0ull, dclock = 0ull;
+  uint32_t dgen = 0u;
+  if (warp == 0) {
+    if (a.covered) {
+      if (lane < a.M) {
+        dtag = a.tag[lane];
+        dstamp = a.stamp[lane];
+        dgen = a.gen[a.slot_base + lane];
+      }
+      dclock = *a.clock;
+    } else if (lane < a.K) {
+      dgen = a.gen[a.staging_base + lane];
+    }
+  }
   griddep_launch_dependents();  // let the expert kernel's CTAs get resident early
-  griddep_wait();               // x and the previous calls' directory writes are visible now
+  griddep_wait();               // x (written by the caller's previous kernel) is visible now
+  if (a.sched_zero && threadIdx.x < 2 * kMaxK) a.sched_zero[threadIdx.x] = 0u;
   if (a.y_zero)                 // the fused expert kernel accumulates the K experts into y
     for (int i = threadIdx.x; i < (a.d >> 2); i += kThreads)
       reinterpret_cast<float4*>(a.y_zero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -121,10 +140,10 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
   unsigned long long clock = 0;
   int nhit = 0, nev = 0;
   if (a.covered) {
-    int32_t tag = lane < M ? a.tag[lane] : -2;
-    unsigned long long st = lane < M ? a.stamp[lane] : 0ull;
-    uint32_t gen = lane < M ? a.gen[a.slot_base + lane] : 0u;
-    clock = *a.clock;
+    int32_t tag = dtag;
+    unsigned long long st = dstamp;
+    uint32_t gen = dgen;
+    clock = dclock;
     // step 1: partition against the pre-access state
     for (int r = 0; r < K; ++r) {
       const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sS[r]);
@@ -181,7 +200,7 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     // beyond coverage: every expert is fetched into a staging slot, never inserted
     if (lane < K) {
       mySlot = a.staging_base + lane;
-      myGen = a.gen[mySlot] + 1u;
+      myGen = dgen + 1u;
       a.gen[mySlot] = myGen;
     }
   }
@@ -244,15 +263,14 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
   }
   __syncwarp();
   if (lane == 0) {
-    // Miss mailbox (host-mapped): an entry is written only when this call missed; the
-    // progress word last_seq is written on every call. A system fence orders the entry
-    // before both words, so last_seq >= seq implies entry(seq) is complete if it exists.
+    // Miss mailbox (host-mapped): an entry is written only when this call missed (payload,
+    // system fence, seq). The progress word is published by the expert kernel at its end
+    // (off this kernel's critical path): progress >= seq implies this kernel completed, so
+    // an entry for seq is visible if it exists.
     if (nmiss) {
       __threadfence_system();
       a.mail->seq = a.seq;
-      __threadfence_system();
     }
-    *a.last_seq = a.seq;
   }
 }
 

@@ -143,6 +143,8 @@ struct moe_ctx {
   FusedPlan plan{};
   int fused_grid = 0;
   unsigned long long* d_bar = nullptr;
+  unsigned* d_ctr = nullptr;  // fused kernel work-claim counters
+  int barmode = 0;
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
@@ -172,8 +174,17 @@ void fetch_thread_main(moe_ctx* c) {
   std::chrono::steady_clock::time_point stop_seen{};
   bool stopping = false;
   while (true) {
-    const unsigned long long last = *c->h_last;  // device progress (every call publishes)
-    if (next > last) {
+    Mail* m = &c->h_mail[next % kMailRing];
+    if (m->seq != next) {
+      // No entry (yet). Once the device progress word reaches `next`, the call's router
+      // kernel has completed, so a missing entry means the call had no miss.
+      if (*c->h_last >= next) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        if (m->seq == next) continue;  // the entry landed between the two reads: process it
+        c->consumed.store(next, std::memory_order_release);
+        ++next;
+        continue;
+      }
       if (c->stop.load()) {
         if (next > c->issued.load()) break;
         if (!stopping) { stopping = true; stop_seen = std::chrono::steady_clock::now(); }
@@ -181,12 +192,6 @@ void fetch_thread_main(moe_ctx* c) {
         if (std::chrono::steady_clock::now() - stop_seen > std::chrono::seconds(5)) break;
       }
       std::this_thread::sleep_for(std::chrono::microseconds(next <= c->issued.load() ? 2 : 20));
-      continue;
-    }
-    Mail* m = &c->h_mail[next % kMailRing];
-    if (m->seq != next) {  // no miss in this call
-      c->consumed.store(next, std::memory_order_release);
-      ++next;
       continue;
     }
     std::atomic_thread_fence(std::memory_order_acquire);
@@ -405,14 +410,27 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMalloc(&c->d_h, sizeof(float) * (size_t)K * c->ffr));
   INIT_TRY(cudaMalloc(&c->d_x_e2e, sizeof(uint16_t) * d));
   INIT_TRY(cudaMalloc(&c->d_y_e2e, sizeof(float) * d));
-  INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * kMaxK));
-  INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * kMaxK));
+  INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * 16 * kMaxK));
+  INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
+  INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * 2 * kMaxK));
+  INIT_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * 2 * kMaxK));
   {
     const char* path = getenv("MOE_EXPERT_PATH");
     const char* pdl = getenv("MOE_PDL");
     c->pdl = !(pdl && pdl[0] == '0');
     c->fused_grid = c->num_sms;
     c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, K, c->fused_grid, &c->plan);
+    if (c->fused) {  // tuning knobs (experiments): W2-row part bytes / bulk copies per part
+      const char* pb = getenv("MOE_FB_PART");
+      const char* cb = getenv("MOE_FB_COPIES");
+      if (pb) {
+        const int v = atoi(pb);
+        if (v >= 16 && v % 16 == 0 && v <= c->plan.SB && (2 * c->ffr + v - 1) / v <= 2) c->plan.partB = v;
+      }
+      if (cb) c->plan.copiesB = atoi(cb) == 2 ? 2 : 1;
+      const char* bm = getenv("MOE_BARMODE");
+      if (bm) c->barmode = atoi(bm);
+    }
     if (getenv("MOE_DEBUG_KERNEL")) {  // progress words in host-mapped memory (slow: PCIe atomics)
       INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
       memset(c->h_dbg, 0, 64);
@@ -475,6 +493,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_x_e2e);
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_bar);
+  cudaFree(c->d_ctr);
   cudaFree(c->d_ts);
   if (c->h_mail) cudaFreeHost(c->h_mail);
   if (c->h_last) cudaFreeHost((void*)c->h_last);
@@ -612,8 +631,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.trace_cap = c->trace_cap;
   ra.token = c->tokens[layer];
   ra.mail = c->d_mail + (seq % kMailRing);
-  ra.last_seq = c->d_last;
   ra.y_zero = (c->fused && c->K == 2) ? y : nullptr;  // the fused kernel reduces the K experts into y
+  ra.sched_zero = c->fused ? c->d_ctr : nullptr;
   ra.seq = seq;
   ra.slot_bytes = c->slot_bytes;
 
@@ -626,6 +645,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ea.h = c->d_h;
   ea.y = y;
   ea.ready = c->d_ready;
+  ea.last_seq = c->d_last;
+  ea.seq = seq;
 
   ProfEv pe;
   prof_begin(c, 0, s, &pe);
@@ -639,10 +660,14 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.e = ea;
     fa.bar = c->d_bar;
     fa.calls = c->fused_calls;
+    fa.ctr = c->d_ctr;
     fa.NS = c->plan.NS;
     fa.SB = c->plan.SB;
     fa.xh_bytes = c->plan.xh_bytes;
     fa.ypart_bytes = c->plan.ypart_bytes;
+    fa.partB = c->plan.partB;
+    fa.copiesB = c->plan.copiesB;
+    fa.barmode = c->barmode;
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
     prof_begin(c, 1, s, &pe);
