@@ -97,7 +97,10 @@ MOE_API moe_status moe_destroy(moe_ctx* ctx);
 typedef enum {
   MOE_POLICY_LRU = 0,          /* P:217 (default; the paper's policy) */
   MOE_POLICY_FIFO = 1,         /* P:218 compared policy: no recency update on a hit */
-  MOE_POLICY_STATIC_RANDOM = 2 /* P:360 analytic baseline: NEXT — returns MOE_ERR_UNSUPPORTED */
+  MOE_POLICY_STATIC_RANDOM = 2 /* P:360 analytic baseline: per covered layer M experts drawn at
+                                  configure time (seeded partial Fisher-Yates over splitmix64(seed ^
+                                  layer<<32 ^ i)), preloaded, never replaced; misses are staged like
+                                  uncovered layers' (no insertion, no eviction). warm_start ignored. */
 } moe_policy;
 
 /* Cache geometry and policy.
@@ -119,7 +122,7 @@ typedef struct {
   int32_t indexes;
   int32_t policy;
   int32_t warm_start;
-  uint64_t seed; /* STATIC_RANDOM only (NEXT) */
+  uint64_t seed; /* STATIC_RANDOM only: seed of the resident draw */
   void* pool;
   int64_t pool_bytes;
 } moe_cache_config;

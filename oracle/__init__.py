@@ -24,7 +24,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-LRU, FIFO = 0, 1
+LRU, FIFO, STATIC = 0, 1, 2
 STAT_FIELDS = ("accesses", "at_least_one_hit", "all_k_hit", "expert_hits", "expert_misses",
                "coverage_misses", "evictions")
 
@@ -48,6 +48,8 @@ def _load():
         lib.oracle_combine.argtypes = [p, p, i32, i32, p]
         lib.oracle_cache_new.argtypes = [i32, i32, i32, i32, i32, i32]
         lib.oracle_cache_new.restype = p
+        lib.oracle_cache_new_seeded.argtypes = [i32, i32, i32, i32, i32, i32, i32, ctypes.c_uint64]
+        lib.oracle_cache_new_seeded.restype = p
         lib.oracle_cache_free.argtypes = [p]
         lib.oracle_cache_access.argtypes = [p, i32, p, p, p, p, p]
         lib.oracle_cache_stats.argtypes = [p, i32, p]
@@ -105,9 +107,12 @@ def combine(o: np.ndarray, w: np.ndarray):
 class Cache:
     """N-index x M-way set-associative expert cache over layers 0..N-1."""
 
-    def __init__(self, L: int, N: int, M: int, K: int, policy: int = LRU, warm_start: bool = False):
+    def __init__(self, L: int, N: int, M: int, K: int, policy: int = LRU, warm_start: bool = False,
+                 n: int = 0, seed: int = 0):
         self.L, self.N, self.M, self.K = L, min(N, L), M, K
-        self._h = _load().oracle_cache_new(L, N, M, K, policy, int(warm_start))
+        if policy == STATIC and n < M:
+            raise ValueError("STATIC policy needs n >= M")
+        self._h = _load().oracle_cache_new_seeded(L, N, M, K, policy, int(warm_start), n, seed)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -159,7 +164,7 @@ RECORD_DTYPE = np.dtype([("token", np.uint32), ("layer", np.uint16), ("rank", np
 
 
 def decode(x: np.ndarray, gates, experts, N: int, M: int, K: int, policy: int = LRU,
-           warm_start: bool = False, tokens=None, compute: bool = True) -> DecodeResult:
+           warm_start: bool = False, tokens=None, compute: bool = True, seed: int = 0) -> DecodeResult:
     """Token-major, layer-ascending decode of decoupled hidden states x[t][l] (R17).
 
     gates[l]  : Wg [n][d] bf16 bits.   experts(l, e) -> (W1, W3, W2) bf16 bits.
@@ -170,7 +175,7 @@ def decode(x: np.ndarray, gates, experts, N: int, M: int, K: int, policy: int = 
     """
     T, L, d = x.shape
     n = gates[0].shape[0]
-    cache = Cache(L, N, M, K, policy, warm_start)
+    cache = Cache(L, N, M, K, policy, warm_start, n=n, seed=seed)
     y = np.zeros((T, L, d), np.float32)
     recs = np.zeros(T * L * K, RECORD_DTYPE)
     z64s = np.zeros((T, L, n), np.float64)

@@ -119,7 +119,17 @@ void oracle_combine(const float* o /* [K][d] */, const float* w, int K, int d, f
  * use; one global recency clock (R21); warm start = experts 0..M-1 in ways
  * 0..M-1 with stamps 1..M (R9).                                                    */
 
-enum { ORACLE_LRU = 0, ORACLE_FIFO = 1 };
+enum { ORACLE_LRU = 0, ORACLE_FIFO = 1, ORACLE_STATIC = 2 };
+
+/* P:360 random static policy: M distinct experts per covered layer, drawn once with a
+ * counter-based generator (partial Fisher-Yates, splitmix64 of seed ^ layer<<32 ^ i), way i
+ * holding the i-th draw; never mutated by accesses. */
+static uint64_t oracle_splitmix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
 
 typedef struct {
   uint64_t accesses, at_least_one_hit, all_k_hit, expert_hits, expert_misses, coverage_misses,
@@ -134,7 +144,15 @@ typedef struct {
   oracle_stats* stats; /* [L] */
 } oracle_cache;
 
+oracle_cache* oracle_cache_new_seeded(int L, int N, int M, int K, int policy, int warm_start, int n,
+                                     uint64_t seed);
+
 oracle_cache* oracle_cache_new(int L, int N, int M, int K, int policy, int warm_start) {
+  return oracle_cache_new_seeded(L, N, M, K, policy, warm_start, 0, 0);
+}
+
+oracle_cache* oracle_cache_new_seeded(int L, int N, int M, int K, int policy, int warm_start, int n,
+                                     uint64_t seed) {
   oracle_cache* c = (oracle_cache*)calloc(1, sizeof(oracle_cache));
   c->L = L; c->N = N < L ? N : L; c->M = M; c->K = K; c->policy = policy;
   c->tag = (int32_t*)malloc(sizeof(int32_t) * (size_t)(c->N > 0 ? c->N : 1) * (size_t)(M > 0 ? M : 1));
@@ -146,6 +164,25 @@ oracle_cache* oracle_cache_new(int L, int N, int M, int K, int policy, int warm_
       c->stamp[s * M + w] = warm_start ? (uint64_t)(w + 1) : 0;
     }
   c->clock = warm_start ? (uint64_t)M : 0;
+  if (policy == ORACLE_STATIC) {
+    int* perm = (int*)malloc(sizeof(int) * (size_t)n);
+    for (int s = 0; s < c->N; ++s) {
+      for (int e = 0; e < n; ++e) perm[e] = e;
+      for (int i = 0; i < M; ++i) {
+        uint64_t z = oracle_splitmix(seed ^ ((uint64_t)(uint32_t)s << 32) ^ (uint64_t)(uint32_t)i);
+        int j = i + (int)(z % (uint64_t)(n - i));
+        int tmp = perm[i];
+        perm[i] = perm[j];
+        perm[j] = tmp;
+      }
+      for (int w = 0; w < M; ++w) {
+        c->tag[s * M + w] = perm[w];
+        c->stamp[s * M + w] = 0;
+      }
+    }
+    free(perm);
+    c->clock = 0;
+  }
   return c;
 }
 
@@ -179,6 +216,15 @@ void oracle_cache_access(oracle_cache* c, int layer, const int32_t* S,
   /* step 2: touch hits in rank order (LRU only; FIFO keeps insertion order) */
   for (int r = 0; r < K; ++r)
     if (hit[r] && c->policy == ORACLE_LRU) stamp[way[r]] = ++c->clock;
+  if (c->policy == ORACLE_STATIC) { /* static residents: misses are never inserted */
+    int nh = 0;
+    for (int r = 0; r < K; ++r) nh += hit[r];
+    st->expert_hits += (uint64_t)nh;
+    st->expert_misses += (uint64_t)(K - nh);
+    if (nh > 0) st->at_least_one_hit++;
+    if (nh == K) st->all_k_hit++;
+    return;
+  }
   /* step 3: insert misses in rank order into the lowest invalid way, else the
    * least-recent way that holds no expert of this access */
   for (int r = 0; r < K; ++r) {

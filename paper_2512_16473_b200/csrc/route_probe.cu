@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
   // before this grid could launch: it can be read before this grid's wait, too.
   int32_t dtag = -2;
   unsigned long long dstamp = 0ull, dclock = 0ull;
-  uint32_t dgen = 0u;
+  uint32_t dgen = 0u, dsgen = 0u;
   if (warp == 0) {
     if (a.covered) {
       if (lane < a.M) {
@@ -78,9 +78,8 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
         dgen = a.gen[a.slot_base + lane];
       }
       dclock = *a.clock;
-    } else if (lane < a.K) {
-      dgen = a.gen[a.staging_base + lane];
     }
+    if (lane < a.K) dsgen = a.gen[a.staging_base + lane];  // staging slot of rank `lane`
   }
   griddep_launch_dependents();  // let the expert kernel's CTAs get resident early
   griddep_wait();               // x (written by the caller's previous kernel) is visible now
@@ -149,7 +148,8 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
       const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sS[r]);
       if (lane == r) { myHit = m != 0u; myWay = m ? __ffs(m) - 1 : -1; }
     }
-    // step 2: touch hits in rank order (LRU; FIFO keeps insertion order)
+    const bool is_static = a.policy == MOE_POLICY_STATIC_RANDOM;
+    // step 2: touch hits in rank order (LRU; FIFO keeps insertion order; STATIC never changes)
     for (int r = 0; r < K; ++r) {
       const int h = __shfl_sync(0xffffffffu, myHit, r);
       const int w = __shfl_sync(0xffffffffu, myWay, r);
@@ -158,8 +158,9 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
         if (lane == w) st = clock;
       }
     }
-    // step 3: insert misses in rank order
-    for (int r = 0; r < K; ++r) {
+    // step 3: insert misses in rank order (STATIC: never; the miss is staged like an
+    // uncovered layer's, "stored in the cache statically")
+    for (int r = 0; r < K && !is_static; ++r) {
       if (__shfl_sync(0xffffffffu, myHit, r)) continue;
       const unsigned inval = __ballot_sync(0xffffffffu, lane < M && tag == -1);
       int v;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
       if (lane == r) { myWay = v; myEv = ev; }
     }
     // write the set back; per-rank slot / generation
-    if (lane < M) {
+    if (lane < M && !is_static) {
       a.tag[lane] = tag;
       a.stamp[lane] = st;
       a.gen[a.slot_base + lane] = gen;
@@ -193,14 +194,20 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     const int wq = myWay < 0 ? 0 : myWay;
     const uint32_t g = __shfl_sync(0xffffffffu, gen, wq);
     if (lane < K) {
-      mySlot = a.slot_base + myWay;
-      myGen = g;
+      if (is_static && !myHit) {
+        mySlot = a.staging_base + lane;
+        myGen = dsgen + 1u;
+        a.gen[mySlot] = myGen;
+      } else {
+        mySlot = a.slot_base + myWay;
+        myGen = g;
+      }
     }
   } else {
     // beyond coverage: every expert is fetched into a staging slot, never inserted
     if (lane < K) {
       mySlot = a.staging_base + lane;
-      myGen = dgen + 1u;
+      myGen = dsgen + 1u;
       a.gen[mySlot] = myGen;
     }
   }

@@ -512,9 +512,7 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   DeviceGuard g(c->device);
   const int M = cfg->ways;
   if (M < c->K || M > c->n) return fail(MOE_ERR_INVALID_ARG, "ways must satisfy K <= M <= n");
-  if (cfg->policy == MOE_POLICY_STATIC_RANDOM)
-    return fail(MOE_ERR_UNSUPPORTED, "STATIC_RANDOM policy is not implemented (NEXT f1)");
-  if (cfg->policy != MOE_POLICY_LRU && cfg->policy != MOE_POLICY_FIFO)
+  if (cfg->policy != MOE_POLICY_LRU && cfg->policy != MOE_POLICY_FIFO && cfg->policy != MOE_POLICY_STATIC_RANDOM)
     return fail(MOE_ERR_INVALID_ARG, "unknown policy");
   long long S;
   int Nraw;
@@ -566,7 +564,33 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   std::vector<unsigned long long> stamp(nways, 0);
   std::vector<uint32_t> gen(nslots, 0);
   unsigned long long clock = 0;
-  if (cfg->warm_start) {
+  if (cfg->policy == MOE_POLICY_STATIC_RANDOM) {
+    // "randomly selecting a set of expert networks to be stored in the cache
+    // statically": per covered layer, M distinct experts drawn with a seeded partial
+    // Fisher-Yates shuffle (counter-based splitmix64 keyed by (seed, layer, i)), way i holds
+    // the i-th draw; loaded once here, never replaced.
+    for (int s = 0; s < Ncov; ++s) {
+      std::vector<int> perm(c->n);
+      for (int e = 0; e < c->n; ++e) perm[e] = e;
+      for (int i = 0; i < M; ++i) {
+        uint64_t z = cfg->seed ^ ((uint64_t)(uint32_t)s << 32) ^ (uint64_t)(uint32_t)i;
+        z += 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const int j = i + (int)(z % (uint64_t)(c->n - i));
+        std::swap(perm[i], perm[j]);
+      }
+      for (int wy = 0; wy < M; ++wy) {
+        tag[(size_t)s * M + wy] = perm[wy];
+        stamp[(size_t)s * M + wy] = 0;
+        gen[(size_t)s * M + wy] = 1;
+        CUDA_TRY(cudaMemcpyAsync(c->pool + ((long long)s * M + wy) * c->slot_bytes,
+                                 c->blobs[(size_t)s * c->n + perm[wy]], (size_t)c->slot_bytes,
+                                 cudaMemcpyHostToDevice, c->fetch_stream));
+      }
+    }
+  } else if (cfg->warm_start) {
     for (int s = 0; s < Ncov; ++s)
       for (int wy = 0; wy < M; ++wy) {
         tag[(size_t)s * M + wy] = wy;

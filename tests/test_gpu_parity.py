@@ -26,11 +26,11 @@ STAT_KEYS = ("accesses", "at_least_one_hit", "all_k_hit", "expert_hits", "expert
              "coverage_misses", "evictions")
 
 
-def _oracle_run(hm, x, N, M, policy=oracle.LRU, warm=False, tokens=None):
+def _oracle_run(hm, x, N, M, policy=oracle.LRU, warm=False, tokens=None, seed=0):
     def experts(l, e):
         return inputs.expert_weights(l, e, hm.d, hm.ff)
     return oracle.decode(x, hm.gates, experts, N=N, M=M, K=hm.K, policy=policy, warm_start=warm,
-                         tokens=tokens)
+                         tokens=tokens, seed=seed)
 
 
 def _compare(hm, m, x, ref, y, tokens=None):
@@ -91,6 +91,18 @@ def test_tiny_geometries_and_policies(tiny, N, M, policy, warm):
             assert m.stats(-1)["coverage_misses"] == 24 * 4 * 2
 
 
+@pytest.mark.parametrize("N,M,seed", [(4, 2, 11), (3, 4, 12), (4, 8, 13)])
+def test_static_random_policy(tiny, N, M, seed):
+    """f1: P:360 random static residents (seeded draw on both sides), misses staged."""
+    x, _ = harness.hidden_states(tiny, 24, "uniform")
+    ref = _oracle_run(tiny, x, N=N, M=M, policy=oracle.STATIC, seed=seed)
+    with harness.open_moe(tiny) as m:
+        m.configure(ways=M, indexes=N, policy=moe.POLICY_STATIC_RANDOM, seed=seed)
+        y = harness.run_decode(m, x)
+        _compare(tiny, m, x, ref, y)
+        assert m.stats(-1)["evictions"] == 0
+
+
 def test_geometry_from_bytes(tiny):
     sb = tiny.slot_bytes
     with harness.open_moe(tiny) as m:
@@ -100,8 +112,7 @@ def test_geometry_from_bytes(tiny):
         assert geo["covered_layers"] == 0
         with pytest.raises(moe.MoeError):
             m.configure(ways=1, indexes=4)                    # M < K rejected (R12)
-        with pytest.raises(moe.MoeError):
-            m.configure(ways=2, indexes=4, policy=moe.POLICY_STATIC_RANDOM)
+
 
 
 @pytest.mark.parametrize("L,d,ff,n,K,M,T", [(3, 200, 136, 16, 3, 5, 20), (2, 72, 40, 32, 1, 2, 30),

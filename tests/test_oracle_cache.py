@@ -227,3 +227,47 @@ def test_generator_forced_repetition_and_paper_preset_band():
     st = inputs.pattern_stats(inputs.generate_trace(8, 8, 2, 1500, inputs.PRESETS["paper"](8)))
     assert 0.40 <= st["token_reuse_at_least_one"] <= 0.70      # P:180 "between 40% and 60%" band
     assert 0.35 <= st["layer_match_at_least_one"] <= 0.55      # P:177 "approximately 44%"
+
+
+# ----------------------------------------------------------------------------- random static policy
+@pytest.mark.parametrize("n,M", [(8, 2), (8, 4), (8, 6), (16, 4), (16, 8)])
+def test_static_random_policy_reaches_paper_closed_forms(n, M):
+    """the random policy stores a random expert set statically; under uniform
+    top-2 routing its hit rates ARE the closed forms (within 0.01 over 1e5)."""
+    rng = np.random.default_rng(77 + n + M)
+    T = 100_000
+    c = oracle.Cache(1, 1, M, 2, oracle.STATIC, n=n, seed=1234 + M)
+    tags0, _ = c.set_state(0)
+    assert len(set(int(t) for t in tags0)) == M and all(0 <= t < n for t in tags0)
+    for _ in range(T):
+        c.access(0, rng.choice(n, size=2, replace=False))
+    tags1, _ = c.set_state(0)
+    assert np.array_equal(tags0, tags1)                 # never mutated (S:260)
+    st = c.stats(0)
+    p1 = 1 - (n - M) / n * (n - M - 1) / (n - 1)
+    p2 = M / n * (M - 1) / (n - 1)
+    assert abs(st["at_least_one_hit"] / T - p1) < 0.01
+    assert abs(st["all_k_hit"] / T - p2) < 0.01
+    assert st["evictions"] == 0 and st["expert_hits"] + st["expert_misses"] == 2 * T
+
+
+def test_static_draw_is_seeded_and_layer_dependent():
+    a = oracle.Cache(4, 4, 3, 2, oracle.STATIC, n=8, seed=5)
+    b = oracle.Cache(4, 4, 3, 2, oracle.STATIC, n=8, seed=5)
+    c = oracle.Cache(4, 4, 3, 2, oracle.STATIC, n=8, seed=6)
+    sets_a = [tuple(a.set_state(l)[0]) for l in range(4)]
+    assert sets_a == [tuple(b.set_state(l)[0]) for l in range(4)]
+    assert sets_a != [tuple(c.set_state(l)[0]) for l in range(4)]
+    assert len(set(sets_a)) > 1
+
+
+def test_lru_beats_static_random_on_paper_pattern_routing():
+    """P:364 (directional): 'LRU improves the probability by around 5~15%' over random."""
+    n, M, K, T = 8, 4, 2, 20000
+    tr = inputs.generate_trace(1, n, K, T, inputs.PRESETS["paper"](n))
+    lru = oracle.Cache(1, 1, M, K)
+    st = oracle.Cache(1, 1, M, K, oracle.STATIC, n=n, seed=3)
+    for t in range(T):
+        lru.access(0, tr[t, 0])
+        st.access(0, tr[t, 0])
+    assert lru.stats(0)["at_least_one_hit"] > st.stats(0)["at_least_one_hit"]
