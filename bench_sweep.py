@@ -37,6 +37,10 @@ def main():
     ap.add_argument("--preset", default="paper")
     ap.add_argument("--check-token", type=int, default=-1, help="token whose y is checked vs the oracle (-1 = last)")
     ap.add_argument("--out", default="")
+    ap.add_argument("--miss-mode", default="fetch", choices=["fetch", "host"],
+                    help="fetch: fill the victim slot then compute on the GPU (B200 design); "
+                         "host: host cores compute the miss while it is post-fetched (paper P:199-201)")
+    ap.add_argument("--host-threads", type=int, default=0)
     args = ap.parse_args()
     import torch
 
@@ -70,7 +74,9 @@ def main():
     for M in [int(v) for v in args.ways.split(",")]:
         ref = oracle.decode(x, hm.gates, None, N=L, M=M, K=c["K"], compute=False)   # routing + cache replay
         with harness.open_moe(hm) as m:
-            geo = m.configure(ways=M, indexes=L)
+            import paper_2512_16473_b200 as moe
+            mm = moe.MISS_HOST_COMPUTE if args.miss_mode == "host" else moe.MISS_FETCH
+            geo = m.configure(ways=M, indexes=L, miss_mode=mm, host_threads=args.host_threads)
             s = torch.cuda.Stream(dev)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             for t in range(T):
@@ -92,14 +98,15 @@ def main():
         n_acc = hits.shape[0]
         timed_fetch = int((rec["hit"] == 0).sum())
         line = {
-            "config": args.config, "layers": L, "ways": M, "indexes": L, "geometry": geo,
+            "config": args.config, "miss_mode": args.miss_mode, "layers": L, "ways": M, "indexes": L,
+            "geometry": geo,
             "tokens_timed": T - 1, "ms": ms, "tokens_per_s": (T - 1) / (ms * 1e-3),
             "ms_per_layer": ms / ((T - 1) * L),
             "hit_rate": {"expert(s)_hit": float((hits.sum(1) > 0).mean()),
                          "all_k_hit": float((hits.sum(1) == c["K"]).mean()),
                          "per_expert": float(hits.mean())},
-            "fetches_timed": timed_fetch,
-            "fetch_gbs": timed_fetch * hm.slot_bytes / (ms * 1e-3) / 1e9,
+            "misses_timed": timed_fetch,
+            "miss_bytes_gbs": timed_fetch * hm.slot_bytes / (ms * 1e-3) / 1e9,
             "stats_all_tokens": st, "trace_bit_exact_vs_oracle": bool(exact),
             "stats_equal_oracle": bool(stats_equal), "accesses_timed": n_acc,
             "build_s": t_build,

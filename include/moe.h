@@ -116,6 +116,20 @@ typedef enum {
  *              The K extra slots stage uncovered-layer experts.
  *  Resets directory, recency clock, stats, trace and token counters. S == 0 is legal:
  *  every layer is uncovered. Synchronizes the device. */
+/* Miss handling.
+ *  MOE_MISS_FETCH (default, the B200 design): a missed expert is copied from pinned host
+ *    memory into its victim slot on the fetch stream and then computed on the GPU (one
+ *    PCIe pass; the same call waits for its fill).
+ *  MOE_MISS_HOST_COMPUTE (the paper's ②(b)/③): the router kernel
+ *    ships x to host memory; the host cores compute the missed expert from the pinned
+ *    backing store while its weights are post-fetched into the victim slot on the fetch
+ *    stream "for future access"; the result comes back on a second (activation) stream and
+ *    the expert kernel adds it. Layers beyond coverage are computed on the host only
+ *    (P:201). A later hit on a slot whose post-fetch has not landed waits for it
+ *    (counted in hit_under_fill). Requires K <= 2 (fused expert kernel). */
+#define MOE_MISS_FETCH 0
+#define MOE_MISS_HOST_COMPUTE 1
+
 typedef struct {
   int64_t cache_bytes;
   int32_t ways;
@@ -125,6 +139,8 @@ typedef struct {
   uint64_t seed; /* STATIC_RANDOM only: seed of the resident draw */
   void* pool;
   int64_t pool_bytes;
+  int32_t miss_mode;    /* MOE_MISS_FETCH | MOE_MISS_HOST_COMPUTE */
+  int32_t host_threads; /* host-compute threads (<= 0: all hardware threads) */
 } moe_cache_config;
 
 typedef struct {
@@ -157,10 +173,13 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* ctx, int32_t layer, const uin
  *  expert_misses includes coverage_misses (layers >= N). fetches / fetch_bytes count
  *  host->device expert copies (one per miss, including staging fills).
  *  hit_under_fill: hits on a slot whose fill had not landed yet at probe time (timing
- *  dependent — not part of the bit-exact contract). */
+ *  dependent — not part of the bit-exact contract; always 0 with MOE_MISS_FETCH, where a
+ *  miss is filled before its own call computes it).
+ *  host_computed: experts computed by the host cores (MOE_MISS_HOST_COMPUTE). In that mode
+ *  fetches count post-fetches (covered misses only). */
 typedef struct {
   uint64_t accesses, at_least_one_hit, all_k_hit, expert_hits, expert_misses, coverage_misses,
-      evictions, fetches, fetch_bytes, hit_under_fill;
+      evictions, fetches, fetch_bytes, hit_under_fill, host_computed;
 } moe_layer_stats;
 
 /* layer in [0, L) or -1 for the sum over layers. Synchronizes the context's streams. */
@@ -206,6 +225,12 @@ typedef struct {
   int32_t expert_path, pdl, ring_stages, stage_bytes, grid, reserved[3];
 } moe_runtime_info;
 MOE_API moe_status moe_get_runtime_info(moe_ctx* ctx, moe_runtime_info* out);
+
+/* The host-CPU expert FFN used by MOE_MISS_HOST_COMPUTE, exposed for testing/benchmarking:
+ * out[d] = W2 (silu(W1 x) * (W3 x)) for one blob in the slot layout (fp32 accumulation,
+ * AVX-512 BF16 when available). threads <= 0: all hardware threads. No GPU needed. */
+MOE_API moe_status moe_host_expert_ffn(const uint16_t* blob, const uint16_t* x, int32_t d, int32_t ffr, float* out,
+                                       int32_t threads);
 
 /* Page-locked host memory for the backing store (cudaHostAlloc, portable): exact size,
  * no power-of-two rounding. Pass already_pinned = 1 in moe_weights for blobs inside it. */

@@ -12,10 +12,10 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (POLICY_FIFO, POLICY_LRU, POLICY_STATIC_RANDOM, PROF_KINDS, RECORD_DTYPE,
-                   STAT_FIELDS)
+from ._abi import (MISS_FETCH, MISS_HOST_COMPUTE, POLICY_FIFO, POLICY_LRU, POLICY_STATIC_RANDOM, PROF_KINDS,
+                   RECORD_DTYPE, STAT_FIELDS)
 
-__all__ = ["Moe", "MoeError", "PinnedBuffer", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
+__all__ = ["Moe", "MoeError", "PinnedBuffer", "MISS_FETCH", "MISS_HOST_COMPUTE", "host_expert_ffn", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
            "STAT_FIELDS", "slot_bytes", "blob_views", "lib", "nccl_unique_id", "PROF_KINDS"]
 
 _lib = None
@@ -74,6 +74,13 @@ class PinnedBuffer:
             self.free()
         except Exception:
             pass
+
+
+def host_expert_ffn(blob: np.ndarray, x: np.ndarray, d: int, ffr: int, threads: int = 0) -> np.ndarray:
+    """The library's host-CPU expert FFN (MOE_MISS_HOST_COMPUTE path) on one blob."""
+    out = np.empty(d, np.float32)
+    _check("moe_host_expert_ffn", lib().moe_host_expert_ffn(_addr(blob), _addr(x), d, ffr, out.ctypes.data, threads))
+    return out
 
 
 def nccl_unique_id() -> bytes:
@@ -142,12 +149,12 @@ class Moe:
     # ------------------------------------------------------------------ cache
     def configure(self, ways: int, indexes: int | None = None, cache_bytes: int | None = None,
                   policy: int = POLICY_LRU, warm_start: bool = False, seed: int = 0,
-                  pool=None, pool_bytes: int = 0) -> dict:
+                  pool=None, pool_bytes: int = 0, miss_mode: int = MISS_FETCH, host_threads: int = 0) -> dict:
         if cache_bytes is None:
             cache_bytes = -1
             indexes = self.L if indexes is None else indexes
         cfg = _abi.CacheConfig(cache_bytes, ways, indexes or 0, policy, int(warm_start), seed,
-                               _addr(pool) if pool is not None else None, pool_bytes)
+                               _addr(pool) if pool is not None else None, pool_bytes, miss_mode, host_threads)
         geo = _abi.CacheGeometry()
         _check("cache_configure", lib().cache_configure(self._h, ctypes.byref(cfg), ctypes.byref(geo)))
         self.geometry = {f: getattr(geo, f) for f, _ in _abi.CacheGeometry._fields_ if f != "reserved"}

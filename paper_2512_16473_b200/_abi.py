@@ -22,7 +22,7 @@ PROF_KINDS = ("route_probe", "expert_ffn", "expert_down", "allreduce")
 EXPORTS = ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward",
            "moe_layer_forward_host", "cache_stats", "cache_trace", "moe_profile_enable",
            "moe_profile_read", "moe_nccl_unique_id", "moe_last_error", "moe_abi_version",
-           "moe_get_runtime_info", "moe_host_alloc", "moe_host_free")
+           "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn")
 
 
 class ModelDesc(ctypes.Structure):
@@ -40,7 +40,8 @@ class Weights(ctypes.Structure):
 class CacheConfig(ctypes.Structure):
     _fields_ = [("cache_bytes", ctypes.c_int64), ("ways", ctypes.c_int32), ("indexes", ctypes.c_int32),
                 ("policy", ctypes.c_int32), ("warm_start", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_int64)]
+                ("pool", ctypes.c_void_p), ("pool_bytes", ctypes.c_int64),
+                ("miss_mode", ctypes.c_int32), ("host_threads", ctypes.c_int32)]
 
 
 class CacheGeometry(ctypes.Structure):
@@ -50,7 +51,8 @@ class CacheGeometry(ctypes.Structure):
 
 
 STAT_FIELDS = ("accesses", "at_least_one_hit", "all_k_hit", "expert_hits", "expert_misses",
-               "coverage_misses", "evictions", "fetches", "fetch_bytes", "hit_under_fill")
+               "coverage_misses", "evictions", "fetches", "fetch_bytes", "hit_under_fill", "host_computed")
+MISS_FETCH, MISS_HOST_COMPUTE = 0, 1
 
 
 class LayerStats(ctypes.Structure):
@@ -93,10 +95,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.moe_get_runtime_info.argtypes = [p, ctypes.POINTER(RuntimeInfo)]
     lib.moe_host_alloc.argtypes = [i64, ctypes.POINTER(p)]
     lib.moe_host_free.argtypes = [p]
+    lib.moe_host_expert_ffn.argtypes = [p, p, i32, i32, p, i32]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_abi_version.restype = i32
     for name in ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward", "moe_layer_forward_host",
                  "cache_stats", "cache_trace", "moe_profile_enable", "moe_profile_read", "moe_nccl_unique_id",
-                 "moe_get_runtime_info", "moe_host_alloc", "moe_host_free"):
+                 "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn"):
         getattr(lib, name).restype = i32
     return lib

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ const uint8_t* sbase;
   __shared__ float swgt;
-  __shared__ int smiss, sslot;
+  __shared__ int swait, shost, sslot;
   __shared__ uint32_t sgen;
   const ExpertArgs& a = f.e;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const int slot = a.route->slot[r];
     sslot = slot;
     sgen = a.route->gen[r];
-    smiss = a.route->miss[r];
+    swait = a.route->wait[r];
+    shost = a.route->host[r];
     sbase = a.pool + (long long)slot * a.slot_bytes;
     swgt = a.route->w[r];
   }
@@ -171,11 +172,40 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __syncthreads();
   const uint8_t* base = sbase;
 
+  if (shost) {
+    // ---------------------------------------------------------------- host-computed expert
+    // (MOE_MISS_HOST_COMPUTE): wait for the host's result on the activation stream
+    // and add w_r * o_r over this CTA's share of y; keep the group barrier count in step.
+    if (threadIdx.x == 0) {
+      red_release_add_u64(f.bar + 16 * r, 1ull);
+      const uint32_t want = (uint32_t)a.seq;
+      const unsigned long long t0 = globaltimer();
+      unsigned ns = 256;
+      while (ld_acquire_u32(a.host_flag + r) != want) {
+        __nanosleep(ns);
+        if (ns < 8192) ns <<= 1;
+        if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+      }
+    }
+    __syncthreads();
+    const int c0 = (int)((long long)d * li / gsz), c1 = (int)((long long)d * (li + 1) / gsz);
+    const float w = swgt;
+    const float* o = a.host_out + (size_t)r * d;
+    for (int c = c0 + (int)threadIdx.x; c < c1; c += kThreadsF) {
+      const float v = w * __ldcg(o + c);
+      if (K == 1) a.y[c] = v;
+      else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
+    }
+    if (b == 0 && threadIdx.x == 0) *a.last_seq = a.seq;
+    griddep_launch_dependents();
+    return;
+  }
+
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      if (smiss) wait_ready(a.ready, sslot, sgen);  // a hit's fill landed in an earlier call
+      if (swait) wait_ready(a.ready, sslot, sgen);  // fill of this slot still in flight
       unsigned* ctrA = f.ctr + r;
       unsigned* ctrB = f.ctr + kMaxK + r;
       uint32_t use = 0;                               // per-stage use-count parity bits

@@ -15,7 +15,7 @@ constexpr int kMailRing = 1024;         // miss-notification mailbox entries (ho
 // Per-layer device counters, same order as moe_layer_stats.
 struct DevStats {
   unsigned long long accesses, at_least_one_hit, all_k_hit, expert_hits, expert_misses,
-      coverage_misses, evictions, fetches, fetch_bytes, hit_under_fill;
+      coverage_misses, evictions, fetches, fetch_bytes, hit_under_fill, host_computed;
 };
 static_assert(sizeof(DevStats) == sizeof(moe_layer_stats), "stats layout");
 
@@ -27,7 +27,8 @@ struct RouteRec {
   float w[kMaxK];
   int32_t slot[kMaxK];   // slot index in the pool (cache way or staging slot)
   uint32_t gen[kMaxK];   // fill generation the slot must reach before it is read
-  int32_t miss[kMaxK];   // 1: filled by this call -> wait for gen; 0: hit, already landed
+  int32_t wait[kMaxK];   // 1: wait until ready[slot] >= gen before reading the slot
+  int32_t host[kMaxK];   // 1: computed by the host cores (MOE_MISS_HOST_COMPUTE miss)
 };
 
 // Miss mailbox entry, in HOST-MAPPED pinned memory, written by the router kernel only for
@@ -40,12 +41,15 @@ struct Mail {
   int32_t expert[kMaxK];
   int32_t slot[kMaxK];
   uint32_t gen[kMaxK];
+  int32_t rank[kMaxK];       // routing rank of the miss
+  int32_t postfetch[kMaxK];  // 1: copy the weights into `slot` (covered miss)
+  int32_t host;              // 1: the host computes these experts (x is in the call's x slot)
 };
 
 struct RouteArgs {
   const uint16_t* Wg;  // [n][d] gate of this layer (device)
   const uint16_t* x;   // [d] (device)
-  int d, n, K, M, layer, covered, policy;
+  int d, n, K, M, layer, covered, policy, miss_mode;
   int32_t* tag;        // [M] set of this layer (covered only)
   unsigned long long* stamp;  // [M]
   int slot_base;       // first slot of this layer's set (= layer * M)
@@ -59,6 +63,7 @@ struct RouteArgs {
   long long trace_idx, trace_cap;
   uint32_t token;
   Mail* mail;          // device alias of the host-mapped ring entry for this call
+  uint16_t* xmail;     // device alias of the host-mapped x slot of this call (host compute)
   unsigned long long seq;
   long long slot_bytes;
   float* y_zero;       // if non-null: zero y[0..d) (the fused expert kernel accumulates into it)
@@ -76,6 +81,8 @@ struct ExpertArgs {
   const uint32_t* ready;
   volatile unsigned long long* last_seq;  // host-mapped progress word, written at the end
   unsigned long long seq;                 // this call's sequence number
+  const float* host_out;                  // [kMaxK][d] host-computed expert outputs (device copy)
+  const uint32_t* host_flag;              // [kMaxK] == (uint32_t)seq once host_out[r] landed
 };
 
 // Fused persistent expert kernel (expert_fused.cu).

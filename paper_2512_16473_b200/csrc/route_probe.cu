@@ -211,9 +211,32 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
       a.gen[mySlot] = myGen;
     }
   }
+  // Miss handling (moe.h): FETCH — the slot (or staging slot) is filled, the expert kernel
+  // waits for it; HOST_COMPUTE — the host computes the missed expert, covered
+  // misses are post-fetched into their victim slot for future calls, and a hit on a slot
+  // whose post-fetch has not landed waits for it (hit-under-fill).
+  const bool hostmode = a.miss_mode == MOE_MISS_HOST_COMPUTE;
+  const bool is_static_pol = a.policy == MOE_POLICY_STATIC_RANDOM;
+  int myWait = 0, myHost = 0, myPost = 0;
+  if (lane < K) {
+    if (myHit) {
+      if (hostmode) myWait = *((volatile const uint32_t*)(a.ready + mySlot)) < myGen;
+    } else if (hostmode) {
+      myHost = 1;
+      myPost = a.covered && !is_static_pol;
+    } else {
+      myWait = 1;
+      myPost = 1;
+    }
+  }
   nhit = __popc(__ballot_sync(0xffffffffu, lane < K && myHit));
   nev = __popc(__ballot_sync(0xffffffffu, lane < K && myEv >= 0));
+  const int nhuf = __popc(__ballot_sync(0xffffffffu, lane < K && myHit && myWait));
+  const int npost = __popc(__ballot_sync(0xffffffffu, lane < K && myPost));
   const unsigned missmask = __ballot_sync(0xffffffffu, lane < K && !myHit);
+  if (hostmode && missmask)  // ship x to host memory for the host-side expert computation
+    for (int i = lane; i < (a.d >> 3); i += 32)
+      reinterpret_cast<int4*>(a.xmail)[i] = reinterpret_cast<const int4*>(a.x)[i];
 
   // ---- route record, trace, mailbox
   if (lane < K) {
@@ -221,7 +244,8 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     a.route->w[lane] = sW[lane];
     a.route->slot[lane] = mySlot;
     a.route->gen[lane] = myGen;
-    a.route->miss[lane] = !myHit;
+    a.route->wait[lane] = myWait;
+    a.route->host[lane] = myHost;
     if (a.trace_idx + lane < a.trace_cap) {
       moe_access_record rec;
       rec.token = a.token;
@@ -241,6 +265,8 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
       a.mail->expert[i] = myS;
       a.mail->slot[i] = mySlot;
       a.mail->gen[i] = myGen;
+      a.mail->rank[i] = lane;
+      a.mail->postfetch[i] = myPost;
     }
   }
   const int nmiss = K - nhit;
@@ -254,18 +280,21 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     if (nhit > 0) atomicAdd(&s->at_least_one_hit, 1ull);
     if (nhit == K) atomicAdd(&s->all_k_hit, 1ull);
     if (nhit) atomicAdd(&s->expert_hits, (unsigned long long)nhit);
-    if (nmiss) {
-      atomicAdd(&s->expert_misses, (unsigned long long)nmiss);
-      atomicAdd(&s->fetches, (unsigned long long)nmiss);
-      atomicAdd(&s->fetch_bytes, (unsigned long long)nmiss * (unsigned long long)a.slot_bytes);
+    if (nmiss) atomicAdd(&s->expert_misses, (unsigned long long)nmiss);
+    if (npost) {
+      atomicAdd(&s->fetches, (unsigned long long)npost);
+      atomicAdd(&s->fetch_bytes, (unsigned long long)npost * (unsigned long long)a.slot_bytes);
     }
+    if (hostmode && nmiss) atomicAdd(&s->host_computed, (unsigned long long)nmiss);
     if (!a.covered) atomicAdd(&s->coverage_misses, (unsigned long long)K);
     if (nev) atomicAdd(&s->evictions, (unsigned long long)nev);
-    // hit_under_fill stays 0 here: a miss is filled before this call's experts are read,
-    // so no later access can find the slot still filling.
+    // hit_under_fill is 0 in FETCH mode by construction: a miss is filled before its own
+    // call reads the slot, so no later access can find it still filling.
+    if (nhuf) atomicAdd(&s->hit_under_fill, (unsigned long long)nhuf);
     if (nmiss) {
       a.mail->layer = a.layer;
       a.mail->nmiss = nmiss;
+      a.mail->host = hostmode;
     }
   }
   __syncwarp();

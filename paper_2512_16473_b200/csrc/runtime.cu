@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "host_expert.h"
 #include "moe_internal.cuh"
 #include "nccl.h"
 
@@ -145,6 +146,15 @@ struct moe_ctx {
   unsigned long long* d_bar = nullptr;
   unsigned* d_ctr = nullptr;  // fused kernel work-claim counters
   int barmode = 0;
+  // MOE_MISS_HOST_COMPUTE: x ring (host-mapped), host outputs, activation stream
+  int miss_mode = MOE_MISS_FETCH;
+  HostExpert* host = nullptr;
+  uint16_t* h_xring = nullptr;
+  uint16_t* d_xring = nullptr;
+  float* h_hout = nullptr;       // pinned [kMaxK][d]
+  float* d_hout = nullptr;       // device [kMaxK][d]
+  uint32_t* d_hflag = nullptr;   // device [kMaxK]
+  cudaStream_t act_stream = nullptr;
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
@@ -196,7 +206,20 @@ void fetch_thread_main(moe_ctx* c) {
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     const int layer = m->layer, nmiss = m->nmiss;
+    auto note = [&](cudaError_t err, CUresult cr) {
+      if ((err != cudaSuccess || cr != CUDA_SUCCESS) && !c->fetch_error.load()) {
+        c->fetch_error_msg = std::string("fetch: ") + cudaGetErrorString(err);
+        c->fetch_error.store(1);
+      }
+    };
+    auto publish = [&](cudaStream_t st, uint32_t* word, uint32_t val) -> CUresult {
+      if (c->write_value32) return c->write_value32((CUstream)st, (CUdeviceptr)word, val, 0);
+      launch_write_ready(word, 0, val, st);
+      return CUDA_SUCCESS;
+    };
+    // weight channel: fills (FETCH) or post-fetches for future calls (HOST_COMPUTE)
     for (int i = 0; i < nmiss; ++i) {
+      if (!m->postfetch[i]) continue;
       const int slot = m->slot[i];
       const int e = m->expert[i];
       const uint32_t gen = m->gen[i];
@@ -206,15 +229,21 @@ void fetch_thread_main(moe_ctx* c) {
                                         c->blobs[(size_t)layer * c->n + e], (size_t)c->slot_bytes,
                                         cudaMemcpyHostToDevice, c->fetch_stream);
       CUresult cr = CUDA_SUCCESS;
-      if (err == cudaSuccess) {
-        if (c->write_value32)
-          cr = c->write_value32((CUstream)c->fetch_stream, (CUdeviceptr)(c->d_ready + slot), gen, 0);
-        else
-          launch_write_ready(c->d_ready, slot, gen, c->fetch_stream);
-      }
-      if ((err != cudaSuccess || cr != CUDA_SUCCESS) && !c->fetch_error.load()) {
-        c->fetch_error_msg = std::string("fetch: ") + cudaGetErrorString(err);
-        c->fetch_error.store(1);
+      if (err == cudaSuccess) cr = publish(c->fetch_stream, c->d_ready + slot, gen);
+      note(err, cr);
+    }
+    // activation channel: the host cores compute the missed experts
+    if (m->host && c->host) {
+      const uint16_t* x = c->h_xring + (size_t)(next % kMailRing) * c->d;
+      for (int i = 0; i < nmiss; ++i) {
+        const int rk = m->rank[i];
+        float* o = c->h_hout + (size_t)rk * c->d;
+        c->host->ffn(c->blobs[(size_t)layer * c->n + m->expert[i]], x, c->d, c->ffr, o);
+        cudaError_t err = cudaMemcpyAsync(c->d_hout + (size_t)rk * c->d, o, sizeof(float) * c->d,
+                                          cudaMemcpyHostToDevice, c->act_stream);
+        CUresult cr = CUDA_SUCCESS;
+        if (err == cudaSuccess) cr = publish(c->act_stream, c->d_hflag + rk, (uint32_t)next);
+        note(err, cr);
       }
     }
     c->consumed.store(next, std::memory_order_release);
@@ -285,6 +314,7 @@ moe_status drain(moe_ctx* c) {
   if (c->any_call) CUDA_TRY(cudaEventSynchronize(c->done_ev));
   while (c->consumed.load(std::memory_order_acquire) < c->issued.load()) std::this_thread::yield();
   CUDA_TRY(cudaStreamSynchronize(c->fetch_stream));
+  if (c->act_stream) CUDA_TRY(cudaStreamSynchronize(c->act_stream));
   if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
   return MOE_OK;
 }
@@ -307,6 +337,14 @@ MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
 
 // Debug only (not in moe.h): host pointer to the mapped kernel progress words, or NULL.
 MOE_API const unsigned* moe_debug_words(moe_ctx* c) { return c ? c->h_dbg : nullptr; }
+
+MOE_API moe_status moe_host_expert_ffn(const uint16_t* blob, const uint16_t* x, int32_t d, int32_t ffr, float* out,
+                                       int32_t threads) {
+  if (!blob || !x || !out || d < 1 || ffr < 1) return fail(MOE_ERR_INVALID_ARG, "bad argument");
+  HostExpert he(threads);
+  he.ffn(blob, x, d, ffr, out);
+  return MOE_OK;
+}
 
 MOE_API moe_status moe_host_alloc(int64_t bytes, void** out) {
   if (!out || bytes <= 0) return fail(MOE_ERR_INVALID_ARG, "bad argument");
@@ -413,6 +451,13 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * 2 * kMaxK));
+  INIT_TRY(cudaHostAlloc((void**)&c->h_xring, sizeof(uint16_t) * (size_t)d * kMailRing, cudaHostAllocMapped));
+  INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_xring, c->h_xring, 0));
+  INIT_TRY(cudaHostAlloc((void**)&c->h_hout, sizeof(float) * (size_t)d * kMaxK, cudaHostAllocDefault));
+  INIT_TRY(cudaMalloc(&c->d_hout, sizeof(float) * (size_t)d * kMaxK));
+  INIT_TRY(cudaMalloc(&c->d_hflag, sizeof(uint32_t) * kMaxK));
+  INIT_TRY(cudaMemset(c->d_hflag, 0, sizeof(uint32_t) * kMaxK));
+  INIT_TRY(cudaStreamCreateWithFlags(&c->act_stream, cudaStreamNonBlocking));
   INIT_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * 2 * kMaxK));
   {
     const char* path = getenv("MOE_EXPERT_PATH");
@@ -481,6 +526,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   c->stop.store(true);
   if (c->fetcher.joinable()) c->fetcher.join();
   if (c->fetch_stream) cudaStreamSynchronize(c->fetch_stream);
+  if (c->act_stream) cudaStreamSynchronize(c->act_stream);
   for (auto& p : c->prof_events) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -494,6 +540,13 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_bar);
   cudaFree(c->d_ctr);
+  cudaFree(c->d_hout);
+  cudaFree(c->d_hflag);
+  if (c->h_xring) cudaFreeHost(c->h_xring);
+  if (c->h_hout) cudaFreeHost(c->h_hout);
+  if (c->act_stream) cudaStreamDestroy(c->act_stream);
+  delete c->host;
+  c->host = nullptr;
   cudaFree(c->d_ts);
   if (c->h_mail) cudaFreeHost(c->h_mail);
   if (c->h_last) cudaFreeHost((void*)c->h_last);
@@ -512,6 +565,10 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   DeviceGuard g(c->device);
   const int M = cfg->ways;
   if (M < c->K || M > c->n) return fail(MOE_ERR_INVALID_ARG, "ways must satisfy K <= M <= n");
+  if (cfg->miss_mode != MOE_MISS_FETCH && cfg->miss_mode != MOE_MISS_HOST_COMPUTE)
+    return fail(MOE_ERR_INVALID_ARG, "unknown miss_mode");
+  if (cfg->miss_mode == MOE_MISS_HOST_COMPUTE && !c->fused)
+    return fail(MOE_ERR_UNSUPPORTED, "MOE_MISS_HOST_COMPUTE needs the fused expert kernel (K <= 2)");
   if (cfg->policy != MOE_POLICY_LRU && cfg->policy != MOE_POLICY_FIFO && cfg->policy != MOE_POLICY_STATIC_RANDOM)
     return fail(MOE_ERR_INVALID_ARG, "unknown policy");
   long long S;
@@ -548,6 +605,9 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   }
   c->M = M; c->Ncov = Ncov; c->Nraw = Nraw; c->S = S; c->nslots = nslots;
   c->policy = cfg->policy; c->pool_bytes = need;
+  c->miss_mode = cfg->miss_mode;
+  if (c->miss_mode == MOE_MISS_HOST_COMPUTE && !c->host) c->host = new HostExpert(cfg->host_threads);
+  CUDA_TRY(cudaMemset(c->d_hflag, 0, sizeof(uint32_t) * kMaxK));
   const long long nways = (long long)(Ncov > 0 ? Ncov : 1) * M;
   CUDA_TRY(cudaMalloc(&c->d_tag, sizeof(int32_t) * nways));
   CUDA_TRY(cudaMalloc(&c->d_stamp, sizeof(unsigned long long) * nways));
@@ -640,7 +700,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.Wg = c->d_gate + (size_t)layer * c->n * c->d;
   ra.x = (const uint16_t*)x;
   ra.d = c->d; ra.n = c->n; ra.K = c->K; ra.M = c->M; ra.layer = layer;
-  ra.covered = covered; ra.policy = c->policy;
+  ra.covered = covered; ra.policy = c->policy; ra.miss_mode = c->miss_mode;
+  ra.xmail = c->d_xring + (size_t)(seq % kMailRing) * c->d;
   ra.tag = covered ? c->d_tag + (size_t)layer * c->M : nullptr;
   ra.stamp = covered ? c->d_stamp + (size_t)layer * c->M : nullptr;
   ra.slot_base = covered ? layer * c->M : 0;
@@ -671,6 +732,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ea.ready = c->d_ready;
   ea.last_seq = c->d_last;
   ea.seq = seq;
+  ea.host_out = c->d_hout;
+  ea.host_flag = c->d_hflag;
 
   ProfEv pe;
   prof_begin(c, 0, s, &pe);

@@ -31,9 +31,9 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_struct_layouts_match_header():
-    assert ctypes.sizeof(_abi.LayerStats) == 80
+    assert ctypes.sizeof(_abi.LayerStats) == 88
     assert _abi.RECORD_DTYPE.itemsize == 20
-    assert ctypes.sizeof(_abi.CacheConfig) == 48
+    assert ctypes.sizeof(_abi.CacheConfig) == 56
     assert ctypes.sizeof(_abi.ModelDesc) == 40
 
 
@@ -68,3 +68,19 @@ def test_slot_layout_helpers():
     assert moe.slot_bytes(4096, 14336) == 352_321_536                 # Mixtral expert ("340 MB")
     assert moe.slot_bytes(4096, 6400) == 157_286_400                  # Phi-3.5-MoE expert ("152 MB")
     assert moe.slot_bytes(6144, 16384, 8) == 603_979_776 // 8
+
+
+@pytest.mark.parametrize("d,ff", [(64, 128), (200, 136), (1024, 512), (4096, 256)])
+def test_host_expert_ffn_matches_oracle(d, ff):
+    """The library's host-CPU expert (MOE_MISS_HOST_COMPUTE) vs the oracle, on CPU."""
+    import inputs
+    import oracle
+    blob = np.empty(3 * d * ff, np.uint16)
+    w1, w3, w2 = moe.blob_views(blob.view(np.uint8), d, ff)
+    inputs.expert_weights_into(w1, w3, w2, 0, 3, d, ff)
+    x = inputs.f32_to_bf16(np.random.default_rng(d).standard_normal(d).astype(np.float32))
+    ref, _ = oracle.expert_ffn(*inputs.expert_weights(0, 3, d, ff), x)
+    for thr in (1, 3):
+        out = moe.host_expert_ffn(blob, x, d, ff, threads=thr)
+        assert np.abs(out - ref).max() <= 1e-5 * np.abs(ref).max()
+    assert np.array_equal(moe.host_expert_ffn(blob, x, d, ff, 1), moe.host_expert_ffn(blob, x, d, ff, 4))
