@@ -1,0 +1,14 @@
+import numpy as np, harness, inputs, oracle, sys
+import paper_2512_16473_b200 as moe
+c = inputs.CONFIGS["tiny"]
+hm = harness.host_model(c["L"], c["d"], c["ff"], c["n"], c["K"])
+x, _ = harness.hidden_states(hm, 6, "paper")
+ref = oracle.decode(x, hm.gates, lambda l, e: inputs.expert_weights(l, e, hm.d, hm.ff), N=3, M=2, K=2)
+for mode in (moe.MISS_FETCH, moe.MISS_HOST_COMPUTE):
+    with harness.open_moe(hm) as m:
+        m.configure(ways=2, indexes=3, miss_mode=mode, host_threads=2)
+        y = harness.run_decode(m, x)
+        tr = m.trace()
+    ok = all(np.array_equal(tr[f].astype(int), ref.records[f].astype(int)) for f in ("expert", "hit", "way", "evicted"))
+    err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()) for t in range(6) for l in range(4))
+    print("mode", mode, "bitexact", ok, "err", err, flush=True)
