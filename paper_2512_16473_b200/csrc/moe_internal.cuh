@@ -2,8 +2,11 @@
 // shared by the runtime (runtime.cu) and the sm_100a kernels (route_probe.cu,
 // expert_gemv.cu). Not part of the ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cuda_bf16.h>
 
 #include "moe.h"
 
@@ -110,6 +113,34 @@ cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid
 cudaError_t preload_fused_kernels();
 
 cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl);
+
+// ---------------------------------------------------------------- prefill (f4, tensor cores)
+constexpr int kPrefillMaxBlk = MOE_MAX_EXPERTS;
+// Device-side plan of one prefill call: the distinct routed experts ("blocks"), each with
+// its tokens gathered into rows [row_off, row_off + 128*mtiles) of X_g / H_g.
+struct PrefillPlan {
+  int nblk, total_mtiles;
+  int row_off[kPrefillMaxBlk];
+  int mt_pref[kPrefillMaxBlk + 1];
+  int slot[kPrefillMaxBlk];
+  int* tok;      // [rows_cap] token of each gathered row (-1 = padding)
+  float* wrow;   // [rows_cap] gate weight of that token for the block's expert
+};
+enum { TC_MODE_PLAIN = 0, TC_MODE_SWIGLU = 1, TC_MODE_DOWN = 2 };
+struct TcArgs {
+  CUtensorMap mapA;   // A operand (K-major rows)
+  CUtensorMap mapB;   // B operand(s) (K-major rows)
+  int mode, M, N, K;  // output rows (PLAIN), output cols, reduction length (multiple of 64)
+  int d, ffr, ldh;
+  float* C;                    // PLAIN: [M][N]
+  __nv_bfloat16* H;            // SWIGLU: H_g rows (ldh = ffr)
+  float* y;                    // DOWN: y [T][d]
+  const PrefillPlan* plan;     // SWIGLU / DOWN
+};
+cudaError_t preload_tc_kernels();
+cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s);
+cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, cudaStream_t s);
+cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, cudaStream_t s);
 void launch_expert_gateup(const ExpertArgs& a, cudaStream_t s, int num_sms);
 void launch_expert_down(const ExpertArgs& a, cudaStream_t s, int num_sms);
 void launch_write_ready(uint32_t* ready, int slot, uint32_t gen, cudaStream_t s);

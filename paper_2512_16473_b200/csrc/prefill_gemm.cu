@@ -1,0 +1,245 @@
+// prefill_gemm.cu — f4: the expert FFN of a batch of T prompt tokens on the 5th-gen
+// tensor cores (sm_100a). Per routed expert e, its tokens X_e [T_e x d] (gathered, padded
+// to 128-row tiles) go through
+//   GEMM1 (fused SwiGLU):  H_e = silu(X_e W1_e^T) * (X_e W3_e^T)      [T_e x ff]   bf16 out
+//   GEMM2 (fused combine): y[token] += w_{token,e} * (H_e W2_e^T)     [T_e x d]    fp32 RED
+// Warp-specialised, one 128 x BN output tile per CTA: warp 4 = TMA producer (2-D tensor
+// maps, 128-B swizzle, mbarrier ring), warp 5 = tcgen05.mma issuer (one elected lane,
+// fp32 accumulators in TMEM, tcgen05.commit frees ring stages), warps 0-3 = epilogue
+// (tcgen05.ld 32x32b, one TMEM lane quarter each). Weights are read straight from the
+// expert cache slots (two tensor maps view the slot pool as rows of d and of ff elements).
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "moe_internal.cuh"
+#include "tc_gemm.cuh"
+
+namespace moe {
+namespace {
+
+using namespace tc;
+
+constexpr int kThreadsTC = 192;
+
+template <int BN, int NB>
+struct TcCfg {
+  static constexpr int kA = BM * BK * 2;          // 16 KB
+  static constexpr int kB = BN * BK * 2;          // 16 / 32 KB
+  static constexpr int kStage = kA + NB * kB;
+  static constexpr int kStages = (kFusedMaxDynSmem - 2048) / kStage > 6 ? 6 : (kFusedMaxDynSmem - 2048) / kStage;
+  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = NB * BN <= 32 ? 32 : NB * BN <= 64 ? 64 : NB * BN <= 128 ? 128 : NB * BN <= 256 ? 256 : 512;
+};
+
+struct TileCoord {
+  int a_row;      // first A row (token row in X_g / H_g, or plain row)
+  int b_row[2];   // first B row of each operand (W1, W3 rows; W2 rows)
+  int out_row;    // output row base (H_g row / y gather row / C row)
+  int out_col;    // output column base
+  int valid;
+};
+
+// Tile of this CTA: blockIdx.x = n tile, blockIdx.y = m tile over all expert blocks.
+__device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN) {
+  TileCoord t;
+  t.valid = 0;
+  const int nt = blockIdx.x, mt = blockIdx.y;
+  if (p.mode == TC_MODE_PLAIN) {
+    t.a_row = mt * BM;
+    t.b_row[0] = nt * BN;
+    t.b_row[1] = 0;
+    t.out_row = mt * BM;
+    t.out_col = nt * BN;
+    t.valid = t.a_row < p.M && t.out_col < p.N;
+    return t;
+  }
+  const PrefillPlan* pl = p.plan;
+  if (mt >= pl->total_mtiles) return t;
+  int blk = 0;
+  while (blk + 1 < pl->nblk && pl->mt_pref[blk + 1] <= mt) ++blk;
+  const int row = pl->row_off[blk] + (mt - pl->mt_pref[blk]) * BM;
+  const long long slot = pl->slot[blk];
+  t.a_row = row;
+  t.out_row = row;
+  t.out_col = nt * BN;
+  if (p.mode == TC_MODE_SWIGLU) {        // B rows in the pool viewed as rows of d elements
+    t.b_row[0] = (int)(slot * 3 * p.ffr + nt * BN);             // W1 rows
+    t.b_row[1] = (int)(slot * 3 * p.ffr + p.ffr + nt * BN);     // W3 rows
+  } else {                                // pool viewed as rows of ffr elements
+    t.b_row[0] = (int)(slot * 3 * p.d + 2 * p.d + nt * BN);     // W2 rows
+    t.b_row[1] = 0;
+  }
+  t.valid = t.out_col < p.N;
+  return t;
+}
+
+template <int BN, int NB>
+__global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_constant__ TcArgs p) {
+  using C = TcCfg<BN, NB>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* accf = empty + C::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileCoord tc = tile_of(p, BN);
+  if (!tc.valid) return;
+  const int ktiles = p.K / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(full + s, 1);
+      ptx::mbar_init(empty + s, 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      prefetch_tmap(&p.mapA);
+      prefetch_tmap(&p.mapB);
+      for (int kb = 0; kb < ktiles; ++kb) {
+        const int s = kb % C::kStages;
+        ptx::mbar_wait(empty + s, ((kb / C::kStages) & 1) ^ 1);
+        uint8_t* st = smem + (size_t)s * C::kStage;
+        ptx::mbar_arrive_expect_tx(full + s, (uint32_t)C::kStage);
+        tma_load_2d(st, &p.mapA, kb * BK, tc.a_row, full + s);
+        for (int j = 0; j < NB; ++j) tma_load_2d(st + C::kA + j * C::kB, &p.mapB, kb * BK, tc.b_row[j], full + s);
+      }
+    }
+  } else if (warp == 5) {
+    // ---------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = umma_idesc_bf16(BM, BN);
+    for (int kb = 0; kb < ktiles; ++kb) {
+      const int s = kb % C::kStages;
+      ptx::mbar_wait(full + s, (kb / C::kStages) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint8_t* st = smem + (size_t)s * C::kStage;
+        const uint64_t da = umma_desc_sw128(st);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) {
+            const uint64_t db = umma_desc_sw128(st + C::kA + j * C::kB);
+            umma_bf16(tmem + j * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          }
+        }
+        umma_commit(empty + s);  // stage free once these MMAs have read it
+      }
+      __syncwarp();
+    }
+    if (lane == 0) umma_commit(accf);  // accumulators complete
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 0-3)
+    ptx::mbar_wait(accf, 0);
+    tc_fence_after();
+    const int row = warp * 32 + lane;                      // accumulator row = TMEM lane
+    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    if (p.mode == TC_MODE_PLAIN) {
+      const int grow = tc.out_row + row;
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + c, v);
+        if (grow < p.M) {
+          float* dst = p.C + (size_t)grow * p.N + tc.out_col + c;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (tc.out_col + c + i < p.N) dst[i] = __uint_as_float(v[i]);
+        }
+      }
+    } else if (p.mode == TC_MODE_SWIGLU) {
+      // h = silu(g) * u  (R4), rounded to bf16 for the second GEMM's A operand
+      const int grow = tc.out_row + row;
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t g[32], u[32];
+        tmem_ld32(tbase + c, g);
+        tmem_ld32(tbase + BN + c, u);
+        __nv_bfloat162 hv[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+          const float h0 = g0 / (1.0f + expf(-g0)) * __uint_as_float(u[i]);
+          const float h1 = g1 / (1.0f + expf(-g1)) * __uint_as_float(u[i + 1]);
+          hv[i / 2] = __floats2bfloat162_rn(h0, h1);
+        }
+        __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.H + (size_t)grow * p.ldh + tc.out_col + c);
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(hv + i);
+      }
+    } else {
+      // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
+      const int tok = p.plan->tok[tc.out_row + row];
+      const float w = p.plan->wrow[tc.out_row + row];
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + c, v);
+        if (tok >= 0 && tc.out_col + c < p.N) {
+          float* dst = p.y + (size_t)tok * p.N + tc.out_col + c;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
+                         "f"(w * __uint_as_float(v[i])), "f"(w * __uint_as_float(v[i + 1])),
+                         "f"(w * __uint_as_float(v[i + 2])), "f"(w * __uint_as_float(v[i + 3]))
+                         : "memory");
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
+  }
+}
+
+template <int BN, int NB>
+cudaError_t launch_tc(const TcArgs& p, int gx, int gy, cudaStream_t s) {
+  using C = TcCfg<BN, NB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  tc_gemm_kernel<BN, NB><<<dim3(gx, gy), kThreadsTC, C::kSmem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t preload_tc_kernels() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<128, 1>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<128, 2>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<256, 1>);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<128, 1>::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<128, 2>::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256, 1>::kSmem);
+  return e;
+}
+
+cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s) {  // C = A B^T, BN = 128
+  return launch_tc<128, 1>(p, (p.N + 127) / 128, (p.M + BM - 1) / BM, s);
+}
+
+cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, cudaStream_t s) {
+  return launch_tc<128, 2>(p, (p.N + 127) / 128, max_mtiles, s);
+}
+
+cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, cudaStream_t s) {
+  return launch_tc<256, 1>(p, (p.N + 255) / 256, max_mtiles, s);
+}
+
+}  // namespace moe

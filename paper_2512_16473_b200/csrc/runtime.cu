@@ -80,6 +80,33 @@ static bool nccl_load(std::string* why) {
 
 // ----------------------------------------------------------------------------- context
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D bf16 tensor map for tcgen05 operands: rows of `inner` elements (row stride
+// row_bytes), box = 64 elements (128 B, one swizzle row) x box_rows, 128-B swizzle.
+static bool encode_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t row_bytes,
+                          uint32_t box_rows) {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    fn = (PFN_encodeTiled)f;
+  }
+  const cuuint64_t dims[2] = {inner, rows};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 struct ProfEv {
   int kind;
@@ -326,6 +353,26 @@ extern "C" {
 
 MOE_API const char* moe_last_error(void) { return g_err.c_str(); }
 MOE_API int32_t moe_abi_version(void) { return MOE_ABI_VERSION; }
+
+// Debug / test only (not in moe.h): C[M][N] = A[M][K] B[N][K]^T on the tcgen05 path (device
+// pointers, bf16 in, fp32 out, K % 64 == 0). Validates descriptors / TMA / TMEM plumbing.
+MOE_API int moe_debug_tc_gemm(const void* A, const void* B, float* C, int M, int N, int K, void* stream) {
+  static bool loaded = false;
+  if (!loaded) {
+    if (preload_tc_kernels() != cudaSuccess) return 3;
+    loaded = true;
+  }
+  if (K % 64 || M < 1 || N < 1) return 1;
+  TcArgs p;
+  memset(&p, 0, sizeof(p));
+  if (!encode_map_2d(&p.mapA, A, (uint64_t)K, (uint64_t)M, (uint64_t)K * 2, 128)) return 2;
+  if (!encode_map_2d(&p.mapB, B, (uint64_t)K, (uint64_t)N, (uint64_t)K * 2, 128)) return 2;
+  p.mode = TC_MODE_PLAIN;
+  p.M = M; p.N = N; p.K = K;
+  p.C = C;
+  cudaError_t e = launch_tc_plain(p, (cudaStream_t)stream);
+  return e == cudaSuccess ? 0 : 3;
+}
 
 // Debug only (not in moe.h): per-CTA timestamps of the last fused launch -> host (grid*8).
 MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
