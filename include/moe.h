@@ -163,6 +163,17 @@ MOE_API moe_status cache_configure(moe_ctx* ctx, const moe_cache_config* cfg, mo
  * runtime thread; the expert kernels wait on the slot's ready generation. */
 MOE_API moe_status moe_layer_forward(moe_ctx* ctx, int32_t layer, const void* x, float* y, void* stream);
 
+/* Prefill (f4): the MoE block for T prompt tokens at once.
+ *  x: DEVICE bf16 [T][d]; y: DEVICE fp32 [T][d] (fully overwritten); both 16-B aligned.
+ * For the cache it is exactly T successive moe_layer_forward calls on the rows of x (same
+ * routing, hit/miss sequence, counters, trace, token indices); the expert FFN runs batched
+ * per distinct routed expert as two tcgen05 tensor-core GEMMs (SwiGLU fused into the first,
+ * the gate-weighted combine into the second; h rounded to bf16 between them, so outputs
+ * differ from the decode path by up to ~1e-3 relative). Requirements (else
+ * MOE_ERR_UNSUPPORTED): full associativity (ways == n), layer covered, MOE_MISS_FETCH,
+ * K <= 2, d % 64 == 0, (ff/P) % 128 == 0. First-touch misses are fetched into their slots. */
+MOE_API moe_status moe_layer_prefill(moe_ctx* ctx, int32_t layer, const void* x, float* y, int32_t T, void* stream);
+
 /* End-to-end variant of moe_layer_forward with HOST buffers: copies x (bf16 [d], best
  * pinned) host->device, runs the layer on the context's own stream, copies y (fp32 [d])
  * device->host and synchronizes. */
@@ -207,8 +218,9 @@ MOE_API moe_status cache_trace(moe_ctx* ctx, moe_access_record* host_out, int64_
  * recorded around every kernel on the launch stream. moe_profile_read synchronizes and
  * returns the accumulated device time (ms) and launch count per kernel class:
  *  0 route_probe (router + cache kernel), 1 expert_ffn (the fused persistent expert
- *  kernel; on the split fallback path: the gate/up kernel), 2 expert_down (split fallback
- *  path only), 3 allreduce (TP). Reading resets. */
+ *  kernel; on the split fallback path: the gate/up kernel; prefill: the SwiGLU tensor-core
+ *  GEMM), 2 expert_down (split fallback path; prefill: the down tensor-core GEMM),
+ *  3 allreduce (TP). Reading resets. */
 #define MOE_PROF_KINDS 4
 typedef struct {
   double ms[MOE_PROF_KINDS];

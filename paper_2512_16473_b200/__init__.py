@@ -166,6 +166,11 @@ class Moe:
         s = stream if isinstance(stream, int) or stream is None else getattr(stream, "cuda_stream", stream)
         _check("moe_layer_forward", lib().moe_layer_forward(self._h, layer, _addr(x), _addr(y), s))
 
+    def prefill(self, layer: int, x, y, T: int, stream=None) -> None:
+        """x: device bf16 [T][d]; y: device fp32 [T][d] (tensor-core batched expert FFN)."""
+        s = stream if isinstance(stream, int) or stream is None else getattr(stream, "cuda_stream", stream)
+        _check("moe_layer_prefill", lib().moe_layer_prefill(self._h, layer, _addr(x), _addr(y), T, s))
+
     def forward_host(self, layer: int, x_host, y_host) -> None:
         _check("moe_layer_forward_host", lib().moe_layer_forward_host(self._h, layer, _addr(x_host), _addr(y_host)))
 

@@ -22,7 +22,8 @@ PROF_KINDS = ("route_probe", "expert_ffn", "expert_down", "allreduce")
 EXPORTS = ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward",
            "moe_layer_forward_host", "cache_stats", "cache_trace", "moe_profile_enable",
            "moe_profile_read", "moe_nccl_unique_id", "moe_last_error", "moe_abi_version",
-           "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn")
+           "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn",
+           "moe_layer_prefill")
 
 
 class ModelDesc(ctypes.Structure):
@@ -96,10 +97,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.moe_host_alloc.argtypes = [i64, ctypes.POINTER(p)]
     lib.moe_host_free.argtypes = [p]
     lib.moe_host_expert_ffn.argtypes = [p, p, i32, i32, p, i32]
+    lib.moe_layer_prefill.argtypes = [p, i32, p, p, i32, p]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_abi_version.restype = i32
     for name in ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward", "moe_layer_forward_host",
                  "cache_stats", "cache_trace", "moe_profile_enable", "moe_profile_read", "moe_nccl_unique_id",
-                 "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn"):
+                 "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn",
+           "moe_layer_prefill"):
         getattr(lib, name).restype = i32
     return lib

@@ -119,13 +119,39 @@ constexpr int kPrefillMaxBlk = MOE_MAX_EXPERTS;
 // Device-side plan of one prefill call: the distinct routed experts ("blocks"), each with
 // its tokens gathered into rows [row_off, row_off + 128*mtiles) of X_g / H_g.
 struct PrefillPlan {
-  int nblk, total_mtiles;
+  int nblk, total_mtiles, rows;
   int row_off[kPrefillMaxBlk];
   int mt_pref[kPrefillMaxBlk + 1];
   int slot[kPrefillMaxBlk];
+  uint32_t gen[kPrefillMaxBlk];
+  int wait[kPrefillMaxBlk];   // 1: the slot is filled by this call -> wait for gen
   int* tok;      // [rows_cap] token of each gathered row (-1 = padding)
   float* wrow;   // [rows_cap] gate weight of that token for the block's expert
 };
+struct PrefillArgs {
+  int T, n, K, M, layer, policy;
+  float* z;                    // [T][n] logits
+  int32_t* tag;                // set of the layer
+  unsigned long long* stamp;
+  int slot_base;
+  uint32_t* gen;
+  unsigned long long* clock;
+  DevStats* stats;
+  int* rt_e;                   // [T][K] routed experts (rank order)
+  float* rt_w;                 // [T][K] gate weights
+  moe_access_record* trace;
+  long long trace_idx, trace_cap;
+  uint32_t token0;
+  Mail* mail;
+  unsigned long long seq;
+  long long slot_bytes;
+  PrefillPlan* plan;
+};
+cudaError_t preload_prefill_kernels();
+cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const uint16_t* x, int d, cudaStream_t s);
+cudaError_t launch_prefill_gather(const uint16_t* x, int d, const PrefillPlan* plan, uint16_t* xg, int rows_cap,
+                                  cudaStream_t s);
+cudaError_t launch_publish_seq(volatile unsigned long long* word, unsigned long long seq, cudaStream_t s);
 enum { TC_MODE_PLAIN = 0, TC_MODE_SWIGLU = 1, TC_MODE_DOWN = 2 };
 struct TcArgs {
   CUtensorMap mapA;   // A operand (K-major rows)
@@ -136,6 +162,7 @@ struct TcArgs {
   __nv_bfloat16* H;            // SWIGLU: H_g rows (ldh = ffr)
   float* y;                    // DOWN: y [T][d]
   const PrefillPlan* plan;     // SWIGLU / DOWN
+  const uint32_t* ready;       // landed fill generation per slot
 };
 cudaError_t preload_tc_kernels();
 cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s);

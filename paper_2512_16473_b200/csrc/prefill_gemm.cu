@@ -32,6 +32,7 @@ struct TcCfg {
 };
 
 struct TileCoord {
+  int blk;        // expert block (prefill modes)
   int a_row;      // first A row (token row in X_g / H_g, or plain row)
   int b_row[2];   // first B row of each operand (W1, W3 rows; W2 rows)
   int out_row;    // output row base (H_g row / y gather row / C row)
@@ -59,6 +60,7 @@ __device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN) {
   while (blk + 1 < pl->nblk && pl->mt_pref[blk + 1] <= mt) ++blk;
   const int row = pl->row_off[blk] + (mt - pl->mt_pref[blk]) * BM;
   const long long slot = pl->slot[blk];
+  t.blk = blk;
   t.a_row = row;
   t.out_row = row;
   t.out_col = nt * BN;
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     if (lane == 0) {
       prefetch_tmap(&p.mapA);
       prefetch_tmap(&p.mapB);
+      if (p.mode != TC_MODE_PLAIN && p.plan->wait[tc.blk])  // expert filled by this call
+        ptx::wait_ready(p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
       for (int kb = 0; kb < ktiles; ++kb) {
         const int s = kb % C::kStages;
         ptx::mbar_wait(empty + s, ((kb / C::kStages) & 1) ^ 1);

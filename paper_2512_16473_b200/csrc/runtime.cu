@@ -182,6 +182,18 @@ struct moe_ctx {
   float* d_hout = nullptr;       // device [kMaxK][d]
   uint32_t* d_hflag = nullptr;   // device [kMaxK]
   cudaStream_t act_stream = nullptr;
+  // prefill (f4) buffers, grown on demand
+  int pf_T = 0, pf_rows = 0;
+  float* d_z = nullptr;
+  int* d_rt_e = nullptr;
+  float* d_rt_w = nullptr;
+  PrefillPlan* d_plan = nullptr;
+  int* d_tok = nullptr;
+  float* d_wrow = nullptr;
+  uint16_t* d_xg = nullptr;
+  uint16_t* d_hg = nullptr;
+  CUtensorMap map_xg{}, map_hg{}, map_pool_d{}, map_pool_f{};
+  bool pool_maps = false;
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
@@ -464,6 +476,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(preload_route_kernels());
   INIT_TRY(preload_expert_kernels());
   INIT_TRY(preload_fused_kernels());
+  INIT_TRY(preload_tc_kernels());
+  INIT_TRY(preload_prefill_kernels());
   INIT_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->blobs.assign(w->expert_blob, w->expert_blob + (size_t)L * n);
   if (!w->already_pinned) {
@@ -589,6 +603,14 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_ctr);
   cudaFree(c->d_hout);
   cudaFree(c->d_hflag);
+  cudaFree(c->d_z);
+  cudaFree(c->d_rt_e);
+  cudaFree(c->d_rt_w);
+  cudaFree(c->d_plan);
+  cudaFree(c->d_tok);
+  cudaFree(c->d_wrow);
+  cudaFree(c->d_xg);
+  cudaFree(c->d_hg);
   if (c->h_xring) cudaFreeHost(c->h_xring);
   if (c->h_hout) cudaFreeHost(c->h_hout);
   if (c->act_stream) cudaStreamDestroy(c->act_stream);
@@ -720,6 +742,7 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   c->trace_count = 0;
   std::fill(c->tokens.begin(), c->tokens.end(), 0u);
   c->configured = true;
+  c->pool_maps = false;
   if (out) {
     out->slots_S = S;
     out->slot_bytes = c->slot_bytes;
@@ -838,6 +861,122 @@ MOE_API moe_status moe_layer_forward(moe_ctx* c, int32_t layer, const void* x, f
   if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
   DeviceGuard g(c->device);
   return forward_impl(c, layer, x, y, (cudaStream_t)stream);
+}
+
+MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, float* y, int32_t T, void* stream) {
+  if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
+  if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
+  if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
+  if (!x || !y || T < 1) return fail(MOE_ERR_INVALID_ARG, "bad x / y / T");
+  if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(MOE_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
+  if (c->M != c->n || layer >= c->Ncov || c->miss_mode != MOE_MISS_FETCH || c->K > 2 || c->d % 64 ||
+      c->ffr % 128 || c->policy == MOE_POLICY_STATIC_RANDOM)
+    return fail(MOE_ERR_UNSUPPORTED,
+                "prefill needs ways == n, a covered layer, MOE_MISS_FETCH, LRU/FIFO, K <= 2, d % 64 == 0, (ff/P) % 128 == 0");
+  if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // ---- buffers (grow on demand) and tensor maps
+  const int rows_cap = ((T * c->K + c->n * 128 + 127) / 128) * 128;
+  if (T > c->pf_T || rows_cap > c->pf_rows) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(c->d_z); cudaFree(c->d_rt_e); cudaFree(c->d_rt_w); cudaFree(c->d_tok); cudaFree(c->d_wrow);
+    cudaFree(c->d_xg); cudaFree(c->d_hg);
+    c->d_z = nullptr; c->d_rt_e = nullptr; c->d_rt_w = nullptr; c->d_tok = nullptr; c->d_wrow = nullptr;
+    c->d_xg = nullptr; c->d_hg = nullptr;
+    c->pf_T = 0; c->pf_rows = 0;
+    CUDA_TRY(cudaMalloc(&c->d_z, sizeof(float) * (size_t)T * c->n));
+    CUDA_TRY(cudaMalloc(&c->d_rt_e, sizeof(int) * (size_t)T * c->K));
+    CUDA_TRY(cudaMalloc(&c->d_rt_w, sizeof(float) * (size_t)T * c->K));
+    CUDA_TRY(cudaMalloc(&c->d_tok, sizeof(int) * (size_t)rows_cap));
+    CUDA_TRY(cudaMalloc(&c->d_wrow, sizeof(float) * (size_t)rows_cap));
+    CUDA_TRY(cudaMalloc(&c->d_xg, sizeof(uint16_t) * (size_t)rows_cap * c->d));
+    CUDA_TRY(cudaMalloc(&c->d_hg, sizeof(uint16_t) * (size_t)rows_cap * c->ffr));
+    if (!c->d_plan) CUDA_TRY(cudaMalloc(&c->d_plan, sizeof(PrefillPlan)));
+    PrefillPlan hp;
+    memset(&hp, 0, sizeof(hp));
+    hp.tok = c->d_tok;
+    hp.wrow = c->d_wrow;
+    CUDA_TRY(cudaMemcpy(c->d_plan, &hp, sizeof(hp), cudaMemcpyHostToDevice));
+    if (!encode_map_2d(&c->map_xg, c->d_xg, c->d, rows_cap, (uint64_t)c->d * 2, 128) ||
+        !encode_map_2d(&c->map_hg, c->d_hg, c->ffr, rows_cap, (uint64_t)c->ffr * 2, 128))
+      return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (prefill buffers)");
+    c->pf_T = T;
+    c->pf_rows = rows_cap;
+  }
+  if (!c->pool_maps) {
+    const uint64_t pool_elems = (uint64_t)c->pool_bytes / 2;
+    if (!encode_map_2d(&c->map_pool_d, c->pool, c->d, pool_elems / c->d, (uint64_t)c->d * 2, 128) ||
+        !encode_map_2d(&c->map_pool_f, c->pool, c->ffr, pool_elems / c->ffr, (uint64_t)c->ffr * 2, 256))
+      return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (slot pool)");
+    c->pool_maps = true;
+  }
+  // host-side back-pressure on the miss mailbox (as in moe_layer_forward)
+  const unsigned long long seq = c->issued.load() + 1;
+  while (seq - c->consumed.load(std::memory_order_acquire) >= (unsigned long long)kMailRing - 1)
+    std::this_thread::yield();
+  // ---- router + cache pass (token order) + plan
+  PrefillArgs pa;
+  pa.T = T; pa.n = c->n; pa.K = c->K; pa.M = c->M; pa.layer = layer; pa.policy = c->policy;
+  pa.z = c->d_z;
+  pa.tag = c->d_tag + (size_t)layer * c->M;
+  pa.stamp = c->d_stamp + (size_t)layer * c->M;
+  pa.slot_base = layer * c->M;
+  pa.gen = c->d_gen;
+  pa.clock = c->d_clock;
+  pa.stats = c->d_stats + layer;
+  pa.rt_e = c->d_rt_e;
+  pa.rt_w = c->d_rt_w;
+  pa.trace = c->d_trace;
+  pa.trace_idx = c->trace_count;
+  pa.trace_cap = c->trace_cap;
+  pa.token0 = c->tokens[layer];
+  pa.mail = c->d_mail + (seq % kMailRing);
+  pa.seq = seq;
+  pa.slot_bytes = c->slot_bytes;
+  pa.plan = c->d_plan;
+  CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(float) * (size_t)T * c->d, s));
+  ProfEv pe;
+  prof_begin(c, 0, s, &pe);
+  CUDA_TRY(launch_prefill_route(pa, c->d_gate + (size_t)layer * c->n * c->d, (const uint16_t*)x, c->d, s));
+  prof_end(c, s, &pe);
+  c->issued.store(seq, std::memory_order_release);
+  c->tokens[layer] += (uint32_t)T;
+  c->trace_count += (long long)T * c->K;
+  CUDA_TRY(launch_prefill_gather((const uint16_t*)x, c->d, c->d_plan, c->d_xg, rows_cap, s));
+  // ---- tensor-core expert FFN: GEMM1 (SwiGLU) then GEMM2 (down + combine)
+  const int max_mtiles = rows_cap / 128;
+  TcArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  ta.d = c->d; ta.ffr = c->ffr; ta.ldh = c->ffr;
+  ta.plan = c->d_plan;
+  ta.ready = c->d_ready;
+  ta.mode = TC_MODE_SWIGLU;
+  ta.mapA = c->map_xg;
+  ta.mapB = c->map_pool_d;
+  ta.N = c->ffr; ta.K = c->d;
+  ta.H = reinterpret_cast<__nv_bfloat16*>(c->d_hg);
+  prof_begin(c, 1, s, &pe);
+  CUDA_TRY(launch_tc_swiglu(ta, max_mtiles, s));
+  prof_end(c, s, &pe);
+  ta.mode = TC_MODE_DOWN;
+  ta.mapA = c->map_hg;
+  ta.mapB = c->map_pool_f;
+  ta.N = c->d; ta.K = c->ffr;
+  ta.y = y;
+  prof_begin(c, 2, s, &pe);
+  CUDA_TRY(launch_tc_down(ta, max_mtiles, s));
+  prof_end(c, s, &pe);
+  if (c->P > 1) {
+    prof_begin(c, 3, s, &pe);
+    ncclResult_t r = g_nccl.AllReduce(y, y, (size_t)T * c->d, ncclFloat32, ncclSum, c->comm, s);
+    prof_end(c, s, &pe);
+    if (r != ncclSuccess) return fail(MOE_ERR_NCCL, "ncclAllReduce failed");
+  }
+  CUDA_TRY(launch_publish_seq(c->d_last, seq, s));
+  CUDA_TRY(cudaEventRecord(c->done_ev, s));
+  c->any_call = true;
+  return MOE_OK;
 }
 
 MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint16_t* x_host, float* y_host) {

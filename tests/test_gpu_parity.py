@@ -359,3 +359,57 @@ def test_host_compute_mixtral_layer_post_fetch_and_hit_under_fill():
         _compare(hm, m, x, ref, y)
         st = m.stats(-1)
         assert st["host_computed"] == st["expert_misses"] and st["fetches"] == st["expert_misses"]
+
+
+def _prefill_run(hm, x, M, warm, policy=moe.POLICY_LRU):
+    import torch
+    T, L, d = x.shape
+    dev = torch.device("cuda", 0)
+    y = torch.empty((L, T, d), dtype=torch.float32, device=dev)
+    with harness.open_moe(hm) as m:
+        m.configure(ways=M, indexes=L, warm_start=warm, policy=policy)
+        for l in range(L):   # layer by layer: the whole prompt of layer l in one call
+            xl = torch.from_numpy(np.ascontiguousarray(x[:, l, :]).view(np.int16)).to(dev)
+            m.prefill(l, xl.data_ptr(), y[l].data_ptr(), T)
+        torch.cuda.synchronize()
+        tr = m.trace()
+        st = [m.stats(l) for l in range(L)]
+    return y.permute(1, 0, 2).cpu().numpy(), tr, st
+
+
+@pytest.mark.parametrize("warm,preset,policy", [(False, "paper", moe.POLICY_LRU), (True, "uniform", moe.POLICY_LRU),
+                                                (False, "uniform", moe.POLICY_FIFO)])
+def test_prefill_tensor_core_path_tiny(tiny, warm, preset, policy):
+    """f4: prompt of T tokens per layer through the tcgen05 GEMMs == T decode calls for the
+    cache (per-layer trace and counters bit-exact) and within the 1e-2 bar for y (h is
+    rounded to bf16 between the two tensor-core GEMMs)."""
+    T = 40
+    x, _ = harness.hidden_states(tiny, T, preset)
+    pol = oracle.LRU if policy == moe.POLICY_LRU else oracle.FIFO
+    ref = _oracle_run(tiny, x, N=tiny.L, M=tiny.n, policy=pol, warm=warm)
+    y, tr, st = _prefill_run(tiny, x, tiny.n, warm, policy)
+    # the prefill trace is layer-major; compare in (token, layer, rank) order
+    order = np.lexsort((tr["rank"], tr["layer"], tr["token"]))
+    got = tr[order]
+    for f in EXACT_FIELDS:
+        np.testing.assert_array_equal(got[f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    for l in range(tiny.L):
+        for k in STAT_KEYS:
+            assert st[l][k] == ref.stats[l][k], (l, k)
+    worst = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
+                for t in range(T) for l in range(tiny.L))
+    assert worst <= TOL, worst
+
+
+@pytest.mark.slow
+def test_prefill_mixtral_layer_256_tokens():
+    c = inputs.CONFIGS["mixtral-8x7b"]
+    hm = harness.host_model(1, c["d"], c["ff"], c["n"], c["K"])
+    T = 256
+    x, _ = harness.hidden_states(hm, T, "paper")
+    ref = _oracle_run(hm, x, N=1, M=c["n"], warm=True)
+    y, tr, st = _prefill_run(hm, x, c["n"], True)
+    for f in EXACT_FIELDS:
+        np.testing.assert_array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    worst = max(float(np.abs(y[t, 0] - ref.y[t, 0]).max() / np.abs(ref.y[t, 0]).max()) for t in range(T))
+    assert worst <= TOL, worst
