@@ -130,7 +130,6 @@ struct PrefillPlan {
 };
 struct PrefillArgs {
   int T, n, K, M, layer, policy;
-  float* z;                    // [T][n] logits
   int32_t* tag;                // set of the layer
   unsigned long long* stamp;
   int slot_base;
@@ -146,7 +145,9 @@ struct PrefillArgs {
   unsigned long long seq;
   long long slot_bytes;
   PrefillPlan* plan;
+  void* scratch;               // prefill_scratch_bytes() of device scratch
 };
+size_t prefill_scratch_bytes();
 cudaError_t preload_prefill_kernels();
 cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const uint16_t* x, int d, cudaStream_t s);
 cudaError_t launch_prefill_gather(const uint16_t* x, int d, const PrefillPlan* plan, uint16_t* xg, int rows_cap,

@@ -6,11 +6,14 @@
 // routed expert on the tensor cores (prefill_gemm.cu). Requires full associativity
 // (M = n, so no expert is evicted inside the batch and every expert keeps one slot).
 //
-//  prefill_logits_kernel  z[t][e] = Wg x_t                     one warp per (t, e)
-//  prefill_cache_kernel   warp 0 walks the tokens in order:    top-K + softmax (R1, R2),
-//                         probe + LRU/FIFO update (R10) exactly as the decode
-//                         router; then the CTA builds the plan: per distinct expert its
-//                         tokens (token order) in 128-row padded blocks, gate weights, slot
+// With M = n nothing is evicted, so the sequential cache semantics decompose into
+// parallel steps (same decisions as the sequential walk; GPU parity tests vs the oracle):
+//  prefill_route_kernel   per token: logits, top-K, softmax, first access key per expert
+//  prefill_plan_kernel    resident experts, ways of first-touch experts in access order,
+//                         fills (mailbox), plan blocks (expert id order, 128-row padded)
+//  prefill_access_kernel  per token: hit = resident before or touched by an earlier token;
+//                         trace, counters, LRU clock of each access (hits then misses)
+//  prefill_lists_kernel   per expert: its tokens in order (block scan), final stamps/clock
 //  prefill_gather_kernel  X_g[row] = x[tok[row]] (zeros on padding rows)
 #include <math.h>
 
@@ -23,226 +26,244 @@ namespace {
 __device__ __forceinline__ float bfl(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bfh(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
-__global__ void __launch_bounds__(256) prefill_logits_kernel(const uint16_t* __restrict__ Wg,
-                                                             const uint16_t* __restrict__ x, int T, int n, int d,
-                                                             float* __restrict__ z) {
-  const int gw = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (gw >= T * n) return;
-  const int t = gw / n, e = gw - t * n;
-  const int4* wr = reinterpret_cast<const int4*>(Wg + (size_t)e * d);
+// Scratch of one prefill call (device), initialised with cudaMemset(0x7f / 0):
+struct PfScratch {
+  int first[MOE_MAX_EXPERTS];                 // first access key t*K + r of expert e (0x7f7f7f7f: none)
+  int cnt[MOE_MAX_EXPERTS];                   // routed (t, r) entries of expert e
+  unsigned long long lastc[MOE_MAX_EXPERTS];  // LRU: clock of the last access of expert e
+  int way[MOE_MAX_EXPERTS];                   // way holding e after the call
+  int isnew[MOE_MAX_EXPERTS];                 // 1: e was not resident before the call (first touch = miss)
+  int newrank[MOE_MAX_EXPERTS];               // order of e among the new experts (by first key)
+  int offs[MOE_MAX_EXPERTS];                  // row offset of e's block in X_g
+  unsigned long long clock0;
+  int nnew;
+};
+
+// (1) one warp per token: logits z = Wg x_t, top-K by (z desc, index asc), softmax over the
+//     K in rank order (exactly the decode router's arithmetic order for the softmax), first
+//     access key and entry count per expert.
+__global__ void __launch_bounds__(256) prefill_route_kernel(const PrefillArgs a, const uint16_t* __restrict__ Wg,
+                                                            const uint16_t* __restrict__ x, int d) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (t >= a.T) return;
+  PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
+  const int n = a.n, K = a.K;
   const int4* xv = reinterpret_cast<const int4*>(x + (size_t)t * d);
-  float acc = 0.f;
-  for (int c = lane; c < (d >> 3); c += 32) {
-    const int4 a = __ldg(wr + c), b = __ldg(xv + c);
-    acc = fmaf(bfl(a.x), bfl(b.x), acc);
-    acc = fmaf(bfh(a.x), bfh(b.x), acc);
-    acc = fmaf(bfl(a.y), bfl(b.y), acc);
-    acc = fmaf(bfh(a.y), bfh(b.y), acc);
-    acc = fmaf(bfl(a.z), bfl(b.z), acc);
-    acc = fmaf(bfh(a.z), bfh(b.z), acc);
-    acc = fmaf(bfl(a.w), bfl(b.w), acc);
-    acc = fmaf(bfh(a.w), bfh(b.w), acc);
-  }
+  float z = -INFINITY;
+  for (int e = 0; e < n; ++e) {
+    const int4* wr = reinterpret_cast<const int4*>(Wg + (size_t)e * d);
+    float acc = 0.f;
+    for (int c = lane; c < (d >> 3); c += 32) {
+      const int4 w4 = __ldg(wr + c), x4 = __ldg(xv + c);
+      acc = fmaf(bfl(w4.x), bfl(x4.x), acc);
+      acc = fmaf(bfh(w4.x), bfh(x4.x), acc);
+      acc = fmaf(bfl(w4.y), bfl(x4.y), acc);
+      acc = fmaf(bfh(w4.y), bfh(x4.y), acc);
+      acc = fmaf(bfl(w4.z), bfl(x4.z), acc);
+      acc = fmaf(bfh(w4.z), bfh(x4.z), acc);
+      acc = fmaf(bfl(w4.w), bfl(x4.w), acc);
+      acc = fmaf(bfh(w4.w), bfh(x4.w), acc);
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) z[(size_t)t * n + e] = acc;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == e) z = acc;
+  }
+  bool taken = lane >= n;
+  int myS = -1;
+  float myZ = 0.f;
+  for (int r = 0; r < K; ++r) {
+    float v = taken ? -INFINITY : z;
+    int idx = taken ? 0x7fffffff : lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    if (lane == idx) taken = true;
+    if (lane == r) { myS = idx; myZ = v; }
+  }
+  const float m = __shfl_sync(0xffffffffu, myZ, 0);
+  float sum = 0.f, mine = 0.f;
+  for (int r = 0; r < K; ++r) {
+    const float e = expf(__shfl_sync(0xffffffffu, myZ, r) - m);
+    sum += e;
+    if (lane == r) mine = e;
+  }
+  if (lane < K) {
+    a.rt_e[(size_t)t * K + lane] = myS;
+    a.rt_w[(size_t)t * K + lane] = mine / sum;
+    atomicMin(&sc->first[myS], t * K + lane);
+    atomicAdd(&sc->cnt[myS], 1);
+  }
 }
 
-__global__ void __launch_bounds__(256) prefill_cache_kernel(const PrefillArgs a) {
-  __shared__ int cnt[MOE_MAX_EXPERTS];
-  __shared__ int offs[MOE_MAX_EXPERTS + 1];
-  __shared__ int bslot[MOE_MAX_EXPERTS];
-  __shared__ uint32_t bgen[MOE_MAX_EXPERTS];
-  __shared__ int bwait[MOE_MAX_EXPERTS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = a.n, K = a.K, M = a.M, T = a.T;
-  if (threadIdx.x < MOE_MAX_EXPERTS) { cnt[threadIdx.x] = 0; bwait[threadIdx.x] = 0; }
-  __syncthreads();
-  if (warp == 0) {
-    // ---- sequential pass in token order: identical decisions to T decode calls
-    int32_t tag = lane < M ? a.tag[lane] : -2;
-    unsigned long long st = lane < M ? a.stamp[lane] : 0ull;
-    uint32_t gen = lane < M ? a.gen[a.slot_base + lane] : 0u;
-    unsigned long long clock = *a.clock;
-    unsigned long long nacc = 0, n1 = 0, nall = 0, nhitt = 0, nmisst = 0, nev = 0;
-    int nmail = 0;
-    for (int t = 0; t < T; ++t) {
-      const float z = lane < n ? a.z[(size_t)t * n + lane] : -INFINITY;
-      bool taken = lane >= n;
-      int myS = -1;
-      float myZ = 0.f;
-      for (int r = 0; r < K; ++r) {
-        float v = taken ? -INFINITY : z;
-        int idx = taken ? 0x7fffffff : lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-          if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
-        }
-        if (lane == idx) taken = true;
-        if (lane == r) { myS = idx; myZ = v; }
-      }
-      // softmax over the K (rank order, fp32): lane 0 computes like the decode router
-      float w = 0.f;
-      {
-        const float m = __shfl_sync(0xffffffffu, myZ, 0);
-        float sum = 0.f, mine = 0.f;
-        for (int r = 0; r < K; ++r) {
-          const float e = expf(__shfl_sync(0xffffffffu, myZ, r) - m);
-          sum += e;
-          if (lane == r) mine = e;
-        }
-        w = mine / sum;
-      }
-      // probe against the pre-access state
-      int myHit = 0, myWay = -1, myEv = -1;
-      for (int r = 0; r < K; ++r) {
-        const int sr = __shfl_sync(0xffffffffu, myS, r);
-        const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sr);
-        if (lane == r) { myHit = m != 0u; myWay = m ? __ffs(m) - 1 : -1; }
-      }
-      for (int r = 0; r < K; ++r) {  // touch hits (LRU)
-        const int h = __shfl_sync(0xffffffffu, myHit, r);
-        const int wv = __shfl_sync(0xffffffffu, myWay, r);
-        if (h && a.policy == MOE_POLICY_LRU) {
-          ++clock;
-          if (lane == wv) st = clock;
-        }
-      }
-      for (int r = 0; r < K; ++r) {  // insert misses (M = n: an invalid way always exists)
-        if (__shfl_sync(0xffffffffu, myHit, r)) continue;
-        const int sr = __shfl_sync(0xffffffffu, myS, r);
-        const unsigned inval = __ballot_sync(0xffffffffu, lane < M && tag == -1);
-        int v;
-        if (inval) {
-          v = __ffs(inval) - 1;
-        } else {  // unreachable with M = n; kept for the general rule (R10)
-          bool pinned = false;
-          for (int q = 0; q < K; ++q) pinned |= (tag == __shfl_sync(0xffffffffu, myS, q));
-          const bool cand = lane < M && !pinned;
-          unsigned long long key = cand ? st : ~0ull;
-          int kl = cand ? lane : 64;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
-            const int ol = __shfl_xor_sync(0xffffffffu, kl, o);
-            if (ok < key || (ok == key && ol < kl)) { key = ok; kl = ol; }
-          }
-          v = kl;
-        }
-        const int ev = __shfl_sync(0xffffffffu, tag, v);
-        ++clock;
-        if (lane == v) { tag = sr; st = clock; ++gen; }
-        if (lane == r) { myWay = v; myEv = ev; }
-      }
-      const int wq = myWay < 0 ? 0 : myWay;
-      const uint32_t g = __shfl_sync(0xffffffffu, gen, wq);
-      const int nh = __popc(__ballot_sync(0xffffffffu, lane < K && myHit));
-      const unsigned missm = __ballot_sync(0xffffffffu, lane < K && !myHit);
-      const int ne = __popc(__ballot_sync(0xffffffffu, lane < K && myEv >= 0));
-      if (lane < K) {
-        a.rt_e[(size_t)t * K + lane] = myS;
-        a.rt_w[(size_t)t * K + lane] = w;
-        const long long ti = a.trace_idx + (long long)t * K + lane;
-        if (ti < a.trace_cap) {
-          moe_access_record rec;
-          rec.token = a.token0 + (uint32_t)t;
-          rec.layer = (uint16_t)a.layer;
-          rec.rank = (uint8_t)lane;
-          rec.hit = (uint8_t)myHit;
-          rec.expert = (int16_t)myS;
-          rec.evicted = (int16_t)myEv;
-          rec.way = (int8_t)myWay;
-          rec.coverage = 0;
-          rec.reserved = 0;
-          rec.weight = w;
-          a.trace[ti] = rec;
-        }
-        if (!myHit) {  // first touch: fill the expert's slot (one mailbox entry per call)
-          const int i = nmail + __popc(missm & ((1u << lane) - 1u));
-          a.mail->expert[i] = myS;
-          a.mail->slot[i] = a.slot_base + myWay;
-          a.mail->gen[i] = g;
-          a.mail->rank[i] = lane;
-          a.mail->postfetch[i] = 1;
-          bwait[myS] = 1;
-        }
-        bslot[myS] = a.slot_base + myWay;
-        bgen[myS] = g;
-        atomicAdd(&cnt[myS], 1);
-      }
-      nmail += __popc(missm);
-      nacc += 1;
-      n1 += nh > 0;
-      nall += nh == K;
-      nhitt += nh;
-      nmisst += K - nh;
-      nev += ne;
-      __syncwarp();
-    }
-    if (lane < M) {
-      a.tag[lane] = tag;
-      a.stamp[lane] = st;
-      a.gen[a.slot_base + lane] = gen;
-    }
-    if (lane == 0) {
-      *a.clock = clock;
-      DevStats* s = a.stats;
-      atomicAdd(&s->accesses, nacc);
-      atomicAdd(&s->at_least_one_hit, n1);
-      atomicAdd(&s->all_k_hit, nall);
-      atomicAdd(&s->expert_hits, nhitt);
-      atomicAdd(&s->expert_misses, nmisst);
-      atomicAdd(&s->fetches, nmisst);
-      atomicAdd(&s->fetch_bytes, nmisst * (unsigned long long)a.slot_bytes);
-      atomicAdd(&s->evictions, nev);
-      if (nmail) {
-        a.mail->layer = a.layer;
-        a.mail->nmiss = nmail;
-        a.mail->host = 0;
-        __threadfence_system();
-        a.mail->seq = a.seq;
-      }
-    }
+// (2) one CTA: which experts are resident, ways for the first-touch experts (lowest invalid
+//     way, in access order — R10 with M = n), fills (mailbox), plan blocks, directory tags.
+__global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
+  PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
+  if (threadIdx.x != 0) return;
+  const int n = a.n, M = a.M;
+  int tag[MOE_MAX_EXPERTS];
+  for (int w = 0; w < M; ++w) tag[w] = a.tag[w];
+  sc->clock0 = *a.clock;
+  int nnew = 0;
+  for (int e = 0; e < n; ++e) {
+    sc->way[e] = -1;
+    sc->isnew[e] = 0;
+    for (int w = 0; w < M; ++w)
+      if (tag[w] == e) sc->way[e] = w;
   }
-  __syncthreads();
-  // ---- plan: distinct experts in id order, 128-row padded blocks
-  if (threadIdx.x == 0) {
-    int nb = 0, off = 0, mt = 0;
-    for (int e = 0; e < n; ++e) {
-      if (!cnt[e]) continue;
-      const int tiles = (cnt[e] + 127) / 128;
-      a.plan->row_off[nb] = off;
-      a.plan->mt_pref[nb] = mt;
-      a.plan->slot[nb] = bslot[e];
-      a.plan->gen[nb] = bgen[e];
-      a.plan->wait[nb] = bwait[e];
-      offs[e] = off;
-      off += tiles * 128;
-      mt += tiles;
-      ++nb;
-    }
+  // first-touch experts in access order (selection by first key; n <= 32)
+  int done[MOE_MAX_EXPERTS];
+  for (int e = 0; e < n; ++e) done[e] = 0;
+  while (true) {
+    int best = -1;
+    for (int e = 0; e < n; ++e)
+      if (!done[e] && sc->cnt[e] > 0 && sc->way[e] < 0 && (best < 0 || sc->first[e] < sc->first[best])) best = e;
+    if (best < 0) break;
+    done[best] = 1;
+    int v = -1;
+    for (int w = 0; w < M && v < 0; ++w)
+      if (tag[w] == -1) v = w;
+    tag[v] = best;
+    sc->way[best] = v;
+    sc->isnew[best] = 1;
+    sc->newrank[best] = nnew;
+    const uint32_t g = a.gen[a.slot_base + v] + 1u;
+    a.gen[a.slot_base + v] = g;
+    a.tag[v] = best;
+    a.mail->expert[nnew] = best;
+    a.mail->slot[nnew] = a.slot_base + v;
+    a.mail->gen[nnew] = g;
+    a.mail->rank[nnew] = 0;
+    a.mail->postfetch[nnew] = 1;
+    ++nnew;
+  }
+  sc->nnew = nnew;
+  // plan: blocks in expert id order, 128-row padded
+  int nb = 0, off = 0, mt = 0;
+  for (int e = 0; e < n; ++e) {
+    if (!sc->cnt[e]) continue;
+    const int tiles = (sc->cnt[e] + 127) / 128;
+    a.plan->row_off[nb] = off;
     a.plan->mt_pref[nb] = mt;
-    a.plan->nblk = nb;
-    a.plan->total_mtiles = mt;
-    a.plan->rows = off;
+    a.plan->slot[nb] = a.slot_base + sc->way[e];
+    a.plan->gen[nb] = a.gen[a.slot_base + sc->way[e]];
+    a.plan->wait[nb] = sc->isnew[e];
+    sc->offs[e] = off;
+    off += tiles * 128;
+    mt += tiles;
+    ++nb;
   }
+  a.plan->mt_pref[nb] = mt;
+  a.plan->nblk = nb;
+  a.plan->total_mtiles = mt;
+  a.plan->rows = off;
+  if (nnew) {
+    a.mail->layer = a.layer;
+    a.mail->nmiss = nnew;
+    a.mail->host = 0;
+    __threadfence_system();
+    a.mail->seq = a.seq;
+  }
+}
+
+// (3) one warp per token: hit/miss (pre-access partition: hit iff resident before the call
+//     or first touched by an earlier token), ways, trace records, counters, LRU clocks
+//     (every access increments the clock: hits of the token first, then its misses, each
+//     in rank order — the decode router's order).
+__global__ void __launch_bounds__(256) prefill_access_kernel(const PrefillArgs a) {
+  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const PfScratch* sc = reinterpret_cast<const PfScratch*>(a.scratch);
+  PfScratch* scw = reinterpret_cast<PfScratch*>(a.scratch);
+  const int K = a.K;
+  int e = -1, hit = 0;
+  if (t < a.T && lane < K) {
+    e = a.rt_e[(size_t)t * K + lane];
+    hit = !sc->isnew[e] || (sc->first[e] / K) < t;
+  }
+  const unsigned hm = __ballot_sync(0xffffffffu, lane < K && hit && t < a.T);
+  const unsigned mm = __ballot_sync(0xffffffffu, lane < K && !hit && t < a.T);
+  if (t < a.T && lane < K) {
+    const int pos = hit ? __popc(hm & ((1u << lane) - 1u)) : __popc(hm) + __popc(mm & ((1u << lane) - 1u));
+    if (a.policy == MOE_POLICY_LRU)
+      atomicMax(&scw->lastc[e], sc->clock0 + (unsigned long long)t * K + pos + 1);
+    const long long ti = a.trace_idx + (long long)t * K + lane;
+    if (ti < a.trace_cap) {
+      moe_access_record rec;
+      rec.token = a.token0 + (uint32_t)t;
+      rec.layer = (uint16_t)a.layer;
+      rec.rank = (uint8_t)lane;
+      rec.hit = (uint8_t)hit;
+      rec.expert = (int16_t)e;
+      rec.evicted = -1;
+      rec.way = (int8_t)sc->way[e];
+      rec.coverage = 0;
+      rec.reserved = 0;
+      rec.weight = a.rt_w[(size_t)t * K + lane];
+      a.trace[ti] = rec;
+    }
+  }
+  // counters: one reduction per warp
+  if (lane == 0 && t < a.T) {
+    const int nh = __popc(hm);
+    DevStats* s = a.stats;
+    atomicAdd(&s->accesses, 1ull);
+    if (nh > 0) atomicAdd(&s->at_least_one_hit, 1ull);
+    if (nh == K) atomicAdd(&s->all_k_hit, 1ull);
+    if (nh) atomicAdd(&s->expert_hits, (unsigned long long)nh);
+    if (K - nh) {
+      atomicAdd(&s->expert_misses, (unsigned long long)(K - nh));
+      atomicAdd(&s->fetches, (unsigned long long)(K - nh));
+      atomicAdd(&s->fetch_bytes, (unsigned long long)(K - nh) * (unsigned long long)a.slot_bytes);
+    }
+  }
+}
+
+// (4) per expert e (one CTA each): its tokens in token order -> rows [offs[e], ...) of the
+//     gathered batch (block-wide scan), padding rows; block 0 also commits recency stamps
+//     and the clock (LRU: clock of each expert's last access; FIFO: insertion order).
+__global__ void __launch_bounds__(1024) prefill_lists_kernel(const PrefillArgs a) {
+  __shared__ int part[1024];
+  const PfScratch* sc = reinterpret_cast<const PfScratch*>(a.scratch);
+  const int e = blockIdx.x, K = a.K, T = a.T;
+  if (e == 0 && threadIdx.x < a.n) {
+    const int ex = threadIdx.x;
+    if (sc->cnt[ex] > 0) {
+      if (a.policy == MOE_POLICY_LRU) a.stamp[sc->way[ex]] = sc->lastc[ex];
+      else if (sc->isnew[ex]) a.stamp[sc->way[ex]] = sc->clock0 + sc->newrank[ex] + 1;
+    }
+    if (threadIdx.x == 0)
+      *a.clock = sc->clock0 + (a.policy == MOE_POLICY_LRU ? (unsigned long long)T * K : (unsigned long long)sc->nnew);
+  }
+  if (e >= a.n || sc->cnt[e] == 0) return;
+  const int per = (T + blockDim.x - 1) / blockDim.x;
+  const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+  int c = 0;
+  for (int t = t0; t < t1; ++t)
+    for (int r = 0; r < K; ++r) c += a.rt_e[(size_t)t * K + r] == e;
+  part[threadIdx.x] = c;
   __syncthreads();
-  if (threadIdx.x < n && cnt[threadIdx.x]) {  // tokens of expert e, in token order
-    const int e = threadIdx.x;
-    int pos = offs[e];
-    for (int t = 0; t < T; ++t)
-      for (int r = 0; r < K; ++r)
-        if (a.rt_e[(size_t)t * K + r] == e) {
-          a.plan->tok[pos] = t;
-          a.plan->wrow[pos] = a.rt_w[(size_t)t * K + r];
-          ++pos;
-        }
-    const int end = offs[e] + ((cnt[e] + 127) / 128) * 128;
-    for (; pos < end; ++pos) {
-      a.plan->tok[pos] = -1;
-      a.plan->wrow[pos] = 0.f;
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // inclusive scan (Hillis-Steele)
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int pos = sc->offs[e] + part[threadIdx.x] - c;
+  for (int t = t0; t < t1; ++t)
+    for (int r = 0; r < K; ++r)
+      if (a.rt_e[(size_t)t * K + r] == e) {
+        a.plan->tok[pos] = t;
+        a.plan->wrow[pos] = a.rt_w[(size_t)t * K + r];
+        ++pos;
+      }
+  if (threadIdx.x == blockDim.x - 1) {
+    const int end = sc->offs[e] + ((sc->cnt[e] + 127) / 128) * 128;
+    for (int p = sc->offs[e] + sc->cnt[e]; p < end; ++p) {
+      a.plan->tok[p] = -1;
+      a.plan->wrow[p] = 0.f;
     }
   }
 }
@@ -269,18 +290,28 @@ cudaError_t launch_publish_seq(volatile unsigned long long* word, unsigned long 
 
 cudaError_t preload_prefill_kernels() {
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, prefill_logits_kernel);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_cache_kernel);
+  cudaError_t e = cudaFuncGetAttributes(&fa, prefill_route_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_plan_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_access_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_lists_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_gather_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, publish_seq_kernel);
   return e;
 }
 
+size_t prefill_scratch_bytes() { return sizeof(PfScratch); }
+
 cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const uint16_t* x, int d,
                                  cudaStream_t s) {
-  const int warps = a.T * a.n;
-  prefill_logits_kernel<<<(warps + 7) / 8, 256, 0, s>>>(Wg, x, a.T, a.n, d, a.z);
-  prefill_cache_kernel<<<1, 256, 0, s>>>(a);
+  // first[] = 0x7f7f7f7f (no access yet), the rest zero
+  cudaError_t e = cudaMemsetAsync(a.scratch, 0, sizeof(PfScratch), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.scratch, 0x7f, sizeof(int) * MOE_MAX_EXPERTS, s);
+  if (e != cudaSuccess) return e;
+  const int blocks = (a.T + 7) / 8;
+  prefill_route_kernel<<<blocks, 256, 0, s>>>(a, Wg, x, d);
+  prefill_plan_kernel<<<1, 32, 0, s>>>(a);
+  prefill_access_kernel<<<blocks, 256, 0, s>>>(a);
+  prefill_lists_kernel<<<a.n, 1024, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -184,7 +184,7 @@ struct moe_ctx {
   cudaStream_t act_stream = nullptr;
   // prefill (f4) buffers, grown on demand
   int pf_T = 0, pf_rows = 0;
-  float* d_z = nullptr;
+  void* d_pfscratch = nullptr;
   int* d_rt_e = nullptr;
   float* d_rt_w = nullptr;
   PrefillPlan* d_plan = nullptr;
@@ -603,7 +603,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_ctr);
   cudaFree(c->d_hout);
   cudaFree(c->d_hflag);
-  cudaFree(c->d_z);
+  cudaFree(c->d_pfscratch);
   cudaFree(c->d_rt_e);
   cudaFree(c->d_rt_w);
   cudaFree(c->d_plan);
@@ -880,12 +880,12 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   const int rows_cap = ((T * c->K + c->n * 128 + 127) / 128) * 128;
   if (T > c->pf_T || rows_cap > c->pf_rows) {
     CUDA_TRY(cudaDeviceSynchronize());
-    cudaFree(c->d_z); cudaFree(c->d_rt_e); cudaFree(c->d_rt_w); cudaFree(c->d_tok); cudaFree(c->d_wrow);
+    cudaFree(c->d_rt_e); cudaFree(c->d_rt_w); cudaFree(c->d_tok); cudaFree(c->d_wrow);
     cudaFree(c->d_xg); cudaFree(c->d_hg);
-    c->d_z = nullptr; c->d_rt_e = nullptr; c->d_rt_w = nullptr; c->d_tok = nullptr; c->d_wrow = nullptr;
+    c->d_rt_e = nullptr; c->d_rt_w = nullptr; c->d_tok = nullptr; c->d_wrow = nullptr;
     c->d_xg = nullptr; c->d_hg = nullptr;
     c->pf_T = 0; c->pf_rows = 0;
-    CUDA_TRY(cudaMalloc(&c->d_z, sizeof(float) * (size_t)T * c->n));
+    if (!c->d_pfscratch) CUDA_TRY(cudaMalloc(&c->d_pfscratch, prefill_scratch_bytes()));
     CUDA_TRY(cudaMalloc(&c->d_rt_e, sizeof(int) * (size_t)T * c->K));
     CUDA_TRY(cudaMalloc(&c->d_rt_w, sizeof(float) * (size_t)T * c->K));
     CUDA_TRY(cudaMalloc(&c->d_tok, sizeof(int) * (size_t)rows_cap));
@@ -918,7 +918,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   // ---- router + cache pass (token order) + plan
   PrefillArgs pa;
   pa.T = T; pa.n = c->n; pa.K = c->K; pa.M = c->M; pa.layer = layer; pa.policy = c->policy;
-  pa.z = c->d_z;
+  pa.scratch = c->d_pfscratch;
   pa.tag = c->d_tag + (size_t)layer * c->M;
   pa.stamp = c->d_stamp + (size_t)layer * c->M;
   pa.slot_base = layer * c->M;
