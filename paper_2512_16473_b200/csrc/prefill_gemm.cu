@@ -28,7 +28,8 @@ struct TcCfg {
   static constexpr int kStage = kA + NB * kB;
   static constexpr int kStages = (kFusedMaxDynSmem - 2048) / kStage > 6 ? 6 : (kFusedMaxDynSmem - 2048) / kStage;
   static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int kTmemCols = NB * BN <= 32 ? 32 : NB * BN <= 64 ? 64 : NB * BN <= 128 ? 128 : NB * BN <= 256 ? 256 : 512;
+  // two accumulator buffers (double-buffered epilogue)
+  static constexpr int kTmemCols = 2 * NB * BN <= 32 ? 32 : 2 * NB * BN <= 64 ? 64 : 2 * NB * BN <= 128 ? 128 : 2 * NB * BN <= 256 ? 256 : 512;
 };
 
 struct TileCoord {
@@ -40,25 +41,40 @@ struct TileCoord {
   int valid;
 };
 
-// Tile of this CTA: blockIdx.x = n tile, blockIdx.y = m tile over all expert blocks.
-__device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN) {
+// Tile enumeration (persistent CTAs take tiles id = blockIdx.x + i * gridDim.x):
+//  PLAIN : m fastest within each n tile.
+//  prefill: expert block, then n tile, then m tile (fastest) — the CTAs working on the m
+//           tiles of one (expert, n tile) run concurrently, so each weight tile is read
+//           from HBM once and re-served from L2.
+__device__ __forceinline__ int num_tiles(const TcArgs& p, int BN) {
+  const int ntn = (p.N + BN - 1) / BN;
+  if (p.mode == TC_MODE_PLAIN) return ntn * ((p.M + BM - 1) / BM);
+  return ntn * p.plan->total_mtiles;
+}
+
+__device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN, int id) {
   TileCoord t;
-  t.valid = 0;
-  const int nt = blockIdx.x, mt = blockIdx.y;
+  t.valid = 1;
+  t.blk = 0;
+  const int ntn = (p.N + BN - 1) / BN;
   if (p.mode == TC_MODE_PLAIN) {
+    const int ntm = (p.M + BM - 1) / BM;
+    const int nt = id / ntm, mt = id - nt * ntm;
     t.a_row = mt * BM;
     t.b_row[0] = nt * BN;
     t.b_row[1] = 0;
     t.out_row = mt * BM;
     t.out_col = nt * BN;
-    t.valid = t.a_row < p.M && t.out_col < p.N;
     return t;
   }
   const PrefillPlan* pl = p.plan;
-  if (mt >= pl->total_mtiles) return t;
+  // expert block of this tile: blocks own ntn * mtiles(blk) consecutive tile ids
   int blk = 0;
-  while (blk + 1 < pl->nblk && pl->mt_pref[blk + 1] <= mt) ++blk;
-  const int row = pl->row_off[blk] + (mt - pl->mt_pref[blk]) * BM;
+  while (blk + 1 < pl->nblk && pl->mt_pref[blk + 1] * ntn <= id) ++blk;
+  const int local = id - pl->mt_pref[blk] * ntn;
+  const int mtiles = pl->mt_pref[blk + 1] - pl->mt_pref[blk];
+  const int nt = local / mtiles, mt = local - nt * mtiles;
+  const int row = pl->row_off[blk] + mt * BM;
   const long long slot = pl->slot[blk];
   t.blk = blk;
   t.a_row = row;
@@ -71,23 +87,27 @@ __device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN) {
     t.b_row[0] = (int)(slot * 3 * p.d + 2 * p.d + nt * BN);     // W2 rows
     t.b_row[1] = 0;
   }
-  t.valid = t.out_col < p.N;
   return t;
 }
 
+// Persistent, warp-specialised: warp 4 = TMA producer, warp 5 = MMA issuer (TMEM owner),
+// warps 0-3 = epilogue. Two accumulator buffers in TMEM: the epilogue of tile i overlaps
+// the main loop of tile i+1.
 template <int BN, int NB>
 __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_constant__ TcArgs p) {
   using C = TcCfg<BN, NB>;
+  constexpr int kAcc = NB * BN;  // TMEM columns of one accumulator buffer
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
   uint64_t* empty = full + C::kStages;
-  uint64_t* accf = empty + C::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* tfull = empty + C::kStages;   // [2] accumulator ready for the epilogue
+  uint64_t* tempty = tfull + 2;           // [2] accumulator drained by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileCoord tc = tile_of(p, BN);
-  if (!tc.valid) return;
+  const int ntiles = num_tiles(p, BN);
+  if ((int)blockIdx.x >= ntiles) return;
   const int ktiles = p.K / BK;
 
   if (threadIdx.x == 0) {
@@ -95,7 +115,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
       ptx::mbar_init(full + s, 1);
       ptx::mbar_init(empty + s, 1);
     }
-    ptx::mbar_init(accf, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(tfull + a, 1);
+      ptx::mbar_init(tempty + a, 4);   // one arrival per epilogue warp
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -109,97 +132,114 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     if (lane == 0) {
       prefetch_tmap(&p.mapA);
       prefetch_tmap(&p.mapB);
-      if (p.mode != TC_MODE_PLAIN && p.plan->wait[tc.blk])  // expert filled by this call
-        ptx::wait_ready(p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
-      for (int kb = 0; kb < ktiles; ++kb) {
-        const int s = kb % C::kStages;
-        ptx::mbar_wait(empty + s, ((kb / C::kStages) & 1) ^ 1);
-        uint8_t* st = smem + (size_t)s * C::kStage;
-        ptx::mbar_arrive_expect_tx(full + s, (uint32_t)C::kStage);
-        tma_load_2d(st, &p.mapA, kb * BK, tc.a_row, full + s);
-        for (int j = 0; j < NB; ++j) tma_load_2d(st + C::kA + j * C::kB, &p.mapB, kb * BK, tc.b_row[j], full + s);
+      int it = 0;  // global k-block counter (ring position)
+      for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
+        const TileCoord tc = tile_of(p, BN, id);
+        if (p.mode != TC_MODE_PLAIN && p.plan->wait[tc.blk])  // expert filled by this call
+          ptx::wait_ready(p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
+        for (int kb = 0; kb < ktiles; ++kb, ++it) {
+          const int s = it % C::kStages;
+          ptx::mbar_wait(empty + s, ((it / C::kStages) & 1) ^ 1);
+          uint8_t* st = smem + (size_t)s * C::kStage;
+          ptx::mbar_arrive_expect_tx(full + s, (uint32_t)C::kStage);
+          tma_load_2d(st, &p.mapA, kb * BK, tc.a_row, full + s);
+          for (int j = 0; j < NB; ++j) tma_load_2d(st + C::kA + j * C::kB, &p.mapB, kb * BK, tc.b_row[j], full + s);
+        }
       }
     }
   } else if (warp == 5) {
     // ---------------------------------------------------------------- MMA issuer
     const uint32_t idesc = umma_idesc_bf16(BM, BN);
-    for (int kb = 0; kb < ktiles; ++kb) {
-      const int s = kb % C::kStages;
-      ptx::mbar_wait(full + s, (kb / C::kStages) & 1);
+    int it = 0, tl = 0;
+    for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++tl) {
+      const int acc = tl & 1;
+      ptx::mbar_wait(tempty + acc, ((tl >> 1) & 1) ^ 1);   // epilogue drained this buffer
       tc_fence_after();
-      if (lane == 0) {
-        const uint8_t* st = smem + (size_t)s * C::kStage;
-        const uint64_t da = umma_desc_sw128(st);
+      const uint32_t tacc = tmem + acc * kAcc;
+      for (int kb = 0; kb < ktiles; ++kb, ++it) {
+        const int s = it % C::kStages;
+        ptx::mbar_wait(full + s, (it / C::kStages) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint8_t* st = smem + (size_t)s * C::kStage;
+          const uint64_t da = umma_desc_sw128(st);
 #pragma unroll
-        for (int k = 0; k < BK / UK; ++k) {
+          for (int k = 0; k < BK / UK; ++k) {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) {
-            const uint64_t db = umma_desc_sw128(st + C::kA + j * C::kB);
-            umma_bf16(tmem + j * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            for (int j = 0; j < NB; ++j) {
+              const uint64_t db = umma_desc_sw128(st + C::kA + j * C::kB);
+              umma_bf16(tacc + j * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            }
           }
+          umma_commit(empty + s);             // stage free once these MMAs have read it
+          if (kb == ktiles - 1) umma_commit(tfull + acc);  // accumulator complete
         }
-        umma_commit(empty + s);  // stage free once these MMAs have read it
+        __syncwarp();
       }
-      __syncwarp();
     }
-    if (lane == 0) umma_commit(accf);  // accumulators complete
-    __syncwarp();
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-3)
-    ptx::mbar_wait(accf, 0);
-    tc_fence_after();
     const int row = warp * 32 + lane;                      // accumulator row = TMEM lane
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
-    if (p.mode == TC_MODE_PLAIN) {
-      const int grow = tc.out_row + row;
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(tbase + c, v);
-        if (grow < p.M) {
-          float* dst = p.C + (size_t)grow * p.N + tc.out_col + c;
+    int tl = 0;
+    for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++tl) {
+      const TileCoord tc = tile_of(p, BN, id);
+      const int acc = tl & 1;
+      ptx::mbar_wait(tfull + acc, (tl >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * kAcc + ((uint32_t)(warp * 32) << 16);
+      if (p.mode == TC_MODE_PLAIN) {
+        const int grow = tc.out_row + row;
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c, v);
+          if (grow < p.M) {
+            float* dst = p.C + (size_t)grow * p.N + tc.out_col + c;
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (tc.out_col + c + i < p.N) dst[i] = __uint_as_float(v[i]);
+            for (int i = 0; i < 32; ++i)
+              if (tc.out_col + c + i < p.N) dst[i] = __uint_as_float(v[i]);
+          }
+        }
+      } else if (p.mode == TC_MODE_SWIGLU) {
+        // h = silu(g) * u  (R4), rounded to bf16 for the second GEMM's A operand
+        const int grow = tc.out_row + row;
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + c, g);
+          tmem_ld32(tbase + BN + c, u);
+          __nv_bfloat162 hv[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
+            const float h0 = g0 / (1.0f + __expf(-g0)) * __uint_as_float(u[i]);
+            const float h1 = g1 / (1.0f + __expf(-g1)) * __uint_as_float(u[i + 1]);
+            hv[i / 2] = __floats2bfloat162_rn(h0, h1);
+          }
+          __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.H + (size_t)grow * p.ldh + tc.out_col + c);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(hv + i);
+        }
+      } else {
+        // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
+        const int tok = p.plan->tok[tc.out_row + row];
+        const float w = p.plan->wrow[tc.out_row + row];
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c, v);
+          if (tok >= 0 && tc.out_col + c < p.N) {
+            float* dst = p.y + (size_t)tok * p.N + tc.out_col + c;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
+                           "f"(w * __uint_as_float(v[i])), "f"(w * __uint_as_float(v[i + 1])),
+                           "f"(w * __uint_as_float(v[i + 2])), "f"(w * __uint_as_float(v[i + 3]))
+                           : "memory");
+          }
         }
       }
-    } else if (p.mode == TC_MODE_SWIGLU) {
-      // h = silu(g) * u  (R4), rounded to bf16 for the second GEMM's A operand
-      const int grow = tc.out_row + row;
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t g[32], u[32];
-        tmem_ld32(tbase + c, g);
-        tmem_ld32(tbase + BN + c, u);
-        __nv_bfloat162 hv[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
-          const float h0 = g0 / (1.0f + expf(-g0)) * __uint_as_float(u[i]);
-          const float h1 = g1 / (1.0f + expf(-g1)) * __uint_as_float(u[i + 1]);
-          hv[i / 2] = __floats2bfloat162_rn(h0, h1);
-        }
-        __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.H + (size_t)grow * p.ldh + tc.out_col + c);
-#pragma unroll
-        for (int i = 0; i < 16; i += 4) *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(hv + i);
-      }
-    } else {
-      // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
-      const int tok = p.plan->tok[tc.out_row + row];
-      const float w = p.plan->wrow[tc.out_row + row];
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(tbase + c, v);
-        if (tok >= 0 && tc.out_col + c < p.N) {
-          float* dst = p.y + (size_t)tok * p.N + tc.out_col + c;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
-                         "f"(w * __uint_as_float(v[i])), "f"(w * __uint_as_float(v[i + 1])),
-                         "f"(w * __uint_as_float(v[i + 2])), "f"(w * __uint_as_float(v[i + 3]))
-                         : "memory");
-        }
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(tempty + acc);
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 5) {
@@ -209,15 +249,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
 }
 
 template <int BN, int NB>
-cudaError_t launch_tc(const TcArgs& p, int gx, int gy, cudaStream_t s) {
+cudaError_t launch_tc(const TcArgs& p, int max_tiles, int num_sms, cudaStream_t s) {
   using C = TcCfg<BN, NB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  tc_gemm_kernel<BN, NB><<<dim3(gx, gy), kThreadsTC, C::kSmem, s>>>(p);
+  const int grid = max_tiles < num_sms ? max_tiles : num_sms;
+  tc_gemm_kernel<BN, NB><<<grid, kThreadsTC, C::kSmem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -235,15 +270,21 @@ cudaError_t preload_tc_kernels() {
 }
 
 cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s) {  // C = A B^T, BN = 128
-  return launch_tc<128, 1>(p, (p.N + 127) / 128, (p.M + BM - 1) / BM, s);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  return launch_tc<128, 1>(p, ((p.N + 127) / 128) * ((p.M + BM - 1) / BM), sms, s);
 }
 
 cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, cudaStream_t s) {
-  return launch_tc<128, 2>(p, (p.N + 127) / 128, max_mtiles, s);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  return launch_tc<128, 2>(p, ((p.N + 127) / 128) * max_mtiles, sms, s);
 }
 
 cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, cudaStream_t s) {
-  return launch_tc<256, 1>(p, (p.N + 255) / 256, max_mtiles, s);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  return launch_tc<256, 1>(p, ((p.N + 255) / 256) * max_mtiles, sms, s);
 }
 
 }  // namespace moe
