@@ -32,7 +32,7 @@ KEYS = {
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
 }
-UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024, "MB": 1024 ** 2, "nsecond": 1e-3, "usecond": 1.0,
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024, "MB": 1024 ** 2, "ms": 1e3, "us": 1.0, "ns": 1e-3, "nsecond": 1e-3, "usecond": 1.0,
               "msecond": 1e3, "%": 1, "": 1}
 
 
