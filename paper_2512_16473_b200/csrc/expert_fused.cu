@@ -154,7 +154,16 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(hbar, 1);
     fence_mbar_init();
   }
-  griddep_wait();  // route record / zeroed y and counters (router kernel), x (caller) visible
+  // The router kernel publishes its route (release) before it completes: acquire it here
+  // instead of waiting for the router grid's completion and memory flush (PDL launch).
+  if (threadIdx.x == 0) {
+    if (a.route_flag) {
+      while (ld_acquire_u64(a.route_flag) != a.seq) {
+      }
+    }
+  }
+  if (!a.route_flag) griddep_wait();
+  __syncthreads();
   if (f.ts && threadIdx.x == 0) f.ts[b * 8 + 1] = globaltimer();
   if (threadIdx.x == 0) {
     const int slot = a.route->slot[r];

@@ -70,6 +70,7 @@ struct RouteArgs {
   unsigned long long seq;
   long long slot_bytes;
   float* y_zero;       // if non-null: zero y[0..d) (the fused expert kernel accumulates into it)
+  unsigned long long* route_flag;  // release-published = seq once the route record is complete
   unsigned* sched_zero;  // if non-null: zero the fused kernel's 2*kMaxK work-claim counters
 };
 
@@ -84,6 +85,7 @@ struct ExpertArgs {
   const uint32_t* ready;
   volatile unsigned long long* last_seq;  // host-mapped progress word, written at the end
   unsigned long long seq;                 // this call's sequence number
+  const unsigned long long* route_flag;   // == seq once the router kernel published the route
   const float* host_out;                  // [kMaxK][d] host-computed expert outputs (device copy)
   const uint32_t* host_flag;              // [kMaxK] == (uint32_t)seq once host_out[r] landed
 };

@@ -298,6 +298,13 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     }
   }
   __syncwarp();
+  if (lane == 0 && a.route_flag) {
+    // Hand the route to the expert kernel without waiting for this grid to complete: the
+    // record, the zeroed y / work counters (written before the CTA barrier) and everything
+    // this grid's griddepcontrol.wait made visible are released at gpu scope.
+    __threadfence();
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.route_flag), "l"(a.seq) : "memory");
+  }
   if (lane == 0) {
     // Miss mailbox (host-mapped): an entry is written only when this call missed (payload,
     // system fence, seq). The progress word is published by the expert kernel at its end

@@ -163,6 +163,7 @@ struct moe_ctx {
   double prof_ms[MOE_PROF_KINDS] = {0, 0, 0, 0};
   uint64_t prof_launches[MOE_PROF_KINDS] = {0, 0, 0, 0};
   cudaEvent_t done_ev = nullptr;
+  cudaEvent_t host_ev = nullptr;  // completion of moe_layer_forward_host
   bool any_call = false;
   // TP
   ncclComm_t comm = nullptr;
@@ -172,6 +173,7 @@ struct moe_ctx {
   int fused_grid = 0;
   unsigned long long* d_bar = nullptr;
   unsigned* d_ctr = nullptr;  // fused kernel work-claim counters
+  unsigned long long* d_route_flag = nullptr;  // router -> expert kernel handoff word
   int barmode = 0;
   // MOE_MISS_HOST_COMPUTE: x ring (host-mapped), host outputs, activation stream
   int miss_mode = MOE_MISS_FETCH;
@@ -495,6 +497,7 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaStreamCreateWithFlags(&c->fetch_stream, cudaStreamNonBlocking));
   INIT_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   INIT_TRY(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
+  INIT_TRY(cudaEventCreateWithFlags(&c->host_ev, cudaEventDisableTiming));
   INIT_TRY(cudaHostAlloc((void**)&c->h_mail, sizeof(Mail) * kMailRing, cudaHostAllocMapped));
   memset((void*)c->h_mail, 0, sizeof(Mail) * kMailRing);
   INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_mail, c->h_mail, 0));
@@ -512,6 +515,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * 2 * kMaxK));
+  INIT_TRY(cudaMalloc(&c->d_route_flag, 128));
+  INIT_TRY(cudaMemset(c->d_route_flag, 0, 128));
   INIT_TRY(cudaHostAlloc((void**)&c->h_xring, sizeof(uint16_t) * (size_t)d * kMailRing, cudaHostAllocMapped));
   INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_xring, c->h_xring, 0));
   INIT_TRY(cudaHostAlloc((void**)&c->h_hout, sizeof(float) * (size_t)d * kMaxK, cudaHostAllocDefault));
@@ -601,6 +606,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_bar);
   cudaFree(c->d_ctr);
+  cudaFree(c->d_route_flag);
   cudaFree(c->d_hout);
   cudaFree(c->d_hflag);
   cudaFree(c->d_pfscratch);
@@ -621,6 +627,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   if (c->h_last) cudaFreeHost((void*)c->h_last);
   for (void* p : c->registered) cudaHostUnregister(p);
   if (c->done_ev) cudaEventDestroy(c->done_ev);
+  if (c->host_ev) cudaEventDestroy(c->host_ev);
   if (c->fetch_stream) cudaStreamDestroy(c->fetch_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -788,6 +795,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.mail = c->d_mail + (seq % kMailRing);
   ra.y_zero = (c->fused && c->K == 2) ? y : nullptr;  // the fused kernel reduces the K experts into y
   ra.sched_zero = c->fused ? c->d_ctr : nullptr;
+  ra.route_flag = c->fused ? c->d_route_flag : nullptr;
   ra.seq = seq;
   ra.slot_bytes = c->slot_bytes;
 
@@ -802,6 +810,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ea.ready = c->d_ready;
   ea.last_seq = c->d_last;
   ea.seq = seq;
+  ea.route_flag = c->fused ? c->d_route_flag : nullptr;
   ea.host_out = c->d_hout;
   ea.host_flag = c->d_hflag;
 
@@ -989,7 +998,13 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint1
   moe_status st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s);
   if (st != MOE_OK) return st;
   CUDA_TRY(cudaMemcpyAsync(y_host, c->d_y_e2e, sizeof(float) * c->d, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
+  // Latency-oriented wait (single-request decode): poll the completion event instead of a
+  // blocking synchronize, whose OS wake-up costs ~10 us per call.
+  CUDA_TRY(cudaEventRecord(c->host_ev, s));
+  cudaError_t q;
+  while ((q = cudaEventQuery(c->host_ev)) == cudaErrorNotReady) {
+  }
+  CUDA_TRY(q);
   return MOE_OK;
 }
 
