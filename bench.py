@@ -269,14 +269,14 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     ffn = prof["expert_ffn"]
     dn = prof["expert_down"]
     rt = prof["route_probe"]
-    fused = dn["launches"] == 0
+    fused = dn["launches"] == 0 and rt["launches"] == 0   # one kernel per step: router inside
     ffn_ms = ffn["ms"] / max(ffn["launches"], 1)
     dn_ms = dn["ms"] / max(dn["launches"], 1)
     rt_ms = rt["ms"] / max(rt["launches"], 1)
-    kname = "expert_fused (gate/up + down + combine)" if fused else "expert_gateup"
-    kbytes = bytes_gateup + bytes_down if fused else bytes_gateup
+    kname = "expert_fused (router + cache probe + gate/up + down + combine)" if fused else "expert_gateup"
+    kbytes = step_bytes if fused else bytes_gateup
     achieved = kbytes / (ffn_ms * 1e-3) / 1e9
-    launches_per_step = 2 if fused else 3
+    launches_per_step = 1 if fused else 3
     traffic = _ncu_traffic()
     clocks = clk.summary()
     line = {
@@ -295,7 +295,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                      "peak_source": peak_src,
                      "step": {"bytes": step_bytes, "gbs": step_bytes / (ms_step * 1e-3) / 1e9,
                               "frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
-                     "kernels_us": {"route_probe": rt_ms * 1e3, "expert_ffn": ffn_ms * 1e3,
+                     "kernels_us": {"route_probe": rt_ms * 1e3 if not fused else None, "expert_ffn": ffn_ms * 1e3,
                                     "expert_down": dn_ms * 1e3 if not fused else None},
                      "profiled_ms_per_step": ms_prof / args.steps},
         "e2e": {"value": e2e_steps / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": d * 2,

@@ -6,17 +6,21 @@
 //
 // Decode batch 1 makes every expert matrix a GEMV (~1 FLOP/byte): an HBM stream, not a
 // tensor-core contraction. Design for B200:
-//  - one CTA per SM (grid = #SMs, cooperative => co-resident). The CTAs are split into K
-//    groups, group r serving routed expert r only: its phase A rows j and its phase B
-//    rows c — 88% in static contiguous blocks, the tail claimed in small chunks from a
-//    per-expert counter (per-SM HBM bandwidth varies by ~10%; stealing evens it out). The
-//    barrier between the phases is per expert (the CTAs that produce h_r), and a CTA needs
-//    only ONE expert's h in shared memory, which leaves room for a large weight ring;
+//  - one CTA per SM (grid = #SMs, cooperative => co-resident). Every CTA works on every
+//    expert, in the order A_o0, A_o1, B_o0, B_o1 (phase A = gate/up rows j, phase B = down
+//    rows c; resident experts before ones still being fetched): 88% of each segment's rows
+//    in static contiguous blocks, the tail claimed in small chunks from a per-segment
+//    counter (per-SM HBM bandwidth varies by ~10%; stealing evens it out over all SMs).
+//    h_r depends on every CTA's phase-A rows of expert r, but B_o0 only starts after
+//    A_o1 has been streamed, so the grid-wide dependency is resolved off the HBM critical
+//    path (per-stage release publications, acquire before the h copy). A CTA needs only
+//    ONE expert's h in shared memory at a time, which leaves room for a large weight ring;
 //  - warp 0 / lane 0 is a producer streaming weight rows with bulk async copies
 //    (cp.async.bulk — the TMA engine's linear path, SASS UBLKCP) into an NS-stage shared
 //    memory ring guarded by full/empty mbarriers (L2 evict-first). Bytes in flight per SM
 //    = the ring (~160 KB at Mixtral shapes), independent of how many consumer warps are
-//    still busy. W2 rows do not depend on h, so the producer streams through the barrier;
+//    still busy. W2 rows do not depend on h, so the producer streams through every
+//    phase and expert switch;
 //  - one consumer warp per ring stage: x (bf16) and then h_r (fp32, stored by phase A in
 //    a 2-plane layout and pulled in with ONE bulk copy) live in shared memory; fp32 FMAs,
 //    warp-shuffle reductions;
@@ -27,6 +31,7 @@
 
 #include "moe_internal.cuh"
 #include "ptx.cuh"
+#include "route_core.cuh"
 
 namespace moe {
 namespace {
@@ -36,6 +41,8 @@ using namespace ptx;
 constexpr int kMaxNS = 10;                 // ring stages (phase B pairs them: NS even)
 constexpr int kWarpsPerStage = 2;          // consumer warps sharing one stage
 constexpr int kThreadsF = 32 * (1 + kWarpsPerStage * kMaxNS);
+constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
+constexpr int kTsPerCta = 40;             // debug timestamps per CTA (MOE_DEBUG_TS)
 
 // Packed fp32 FMA (sm_100: FFMA2): acc.{x,y} += a.{x,y} * b.{x,y}
 __device__ __forceinline__ float2 ffma2(const float2 a, const float2 b, const float2 c) {
@@ -45,6 +52,28 @@ __device__ __forceinline__ float2 ffma2(const float2 a, const float2 b, const fl
       : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)),
         "l"(*reinterpret_cast<const unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&r);
+}
+
+// acc.{x,y} += w.{lo,hi} * x.{lo,hi}: sm_100 mixed-precision FMA (SASS FHFMA.BF16, the
+// halves selected in the instruction), bf16 products exact in fp32, one rounding per step
+__device__ __forceinline__ float2 fma_bf16x2(const uint32_t w, const uint32_t x, float2 acc) {
+  asm("{\n\t.reg .b16 wl, wh, xl, xh;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "mov.b32 {xl, xh}, %3;\n\t"
+      "fma.rn.f32.bf16 %0, wl, xl, %0;\n\t"
+      "fma.rn.f32.bf16 %1, wh, xh, %1;\n\t}"
+      : "+f"(acc.x), "+f"(acc.y)
+      : "r"(w), "r"(x));
+  return acc;
+}
+
+// acc += w(8 bf16) . x(8 bf16)
+__device__ __forceinline__ float2 dot8_bf(const int4 w, const int4 x, float2 acc) {
+  acc = fma_bf16x2((uint32_t)w.x, (uint32_t)x.x, acc);
+  acc = fma_bf16x2((uint32_t)w.y, (uint32_t)x.y, acc);
+  acc = fma_bf16x2((uint32_t)w.z, (uint32_t)x.z, acc);
+  acc = fma_bf16x2((uint32_t)w.w, (uint32_t)x.w, acc);
+  return acc;
 }
 
 // bf16 pair (one 32-bit word) -> (lo, hi) fp32, exact
@@ -81,26 +110,33 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
 
 constexpr int kChunkA = 2;     // phase A rows per tail claim
 constexpr int kChunkB = 1;     // phase B rows per tail claim
-constexpr int kStaticPct = 88; // share of each phase's rows assigned statically (no atomics)
+constexpr int kStaticPct = 88; // share of each segment's rows assigned statically (no atomics)
 
-// Static-then-steal schedule over `total` rows for CTA li of a group of gsz CTAs: the first
-// kStaticPct% of the rows are split into equal contiguous blocks, the tail is claimed in
-// chunks from a per-expert counter, so every CTA of the group ends each phase within about
-// one chunk of the others, whatever its share of HBM bandwidth.
+// Ring-slot meta word: >= 0 a weight row (phase A: (r << 24) | j, phase B: c);
+// kEnd closes a phase; kSegB switches phase B to the next expert; kSegA - r closes
+// phase-A segment r in this stage (its h writer publishes the rows it wrote).
+constexpr int kEnd = -1;
+constexpr int kSegB = -2;
+constexpr int kSegA = -3;
+
+// Static-then-steal schedule over `total` rows for CTA b of G: the first kStaticPct% of
+// the rows are split into equal contiguous blocks, the tail is claimed in chunks from a
+// per-segment counter, so every CTA ends each segment within about one chunk of the
+// others, whatever its share of HBM bandwidth.
 struct RowSched {
   int s0, s1;    // this CTA's static block
   int tail0;     // first tail row
 };
-__device__ __forceinline__ RowSched make_sched(int total, int li, int gsz) {
+__device__ __forceinline__ RowSched make_sched(int total, int b, int G) {
   RowSched rs;
-  const int sb = (int)((long long)total * kStaticPct / 100 / gsz);
-  rs.s0 = li * sb;
+  const int sb = (int)((long long)total * kStaticPct / 100 / G);
+  rs.s0 = b * sb;
   rs.s1 = rs.s0 + sb;
-  rs.tail0 = gsz * sb;
+  rs.tail0 = G * sb;
   return rs;
 }
 
-// Shared memory: ring[NS][SB] | xh | full[NS] empty[NS] hbar | meta[NS] | part[NS][2] |
+// Shared memory: ring[NS][SB] | xh | full[NS] empty[NS] hbar | meta[NS] | part[NS][4] |
 //                parB[NS/2]
 //  - phase A: stage s (16 KB) = one W1 row + one W3 row, consumed by warps 2s, 2s+1 (one
 //    half of the row each); x lives in xh as fp32.
@@ -111,13 +147,24 @@ __device__ __forceinline__ RowSched make_sched(int total, int li, int gsz) {
 //    (deterministic, no atomics). Every consumer warp waits on one mbarrier per phase, and
 //    its next wait is always one phase ahead of the part it just released: parity waits
 //    cannot alias.
+//
+// Work order (all CTAs, no group split): phase A of every device-computed expert in turn
+// (A_o0, A_o1), then phase B (B_o0, B_o1). h_r is complete once every stage of every CTA
+// has passed the kSegA marker that closes A_r; each stage's single h writer publishes its
+// own rows then (release RED on bar[r]). B_o0 starts only after A_o1 has streamed, so its
+// wait on bar[o0] is normally already satisfied: the grid-wide dependency costs no HBM time.
 __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedArgs f) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ const uint8_t* sbase;
-  __shared__ float swgt;
-  __shared__ int swait, shost, sslot;
-  __shared__ uint32_t sgen;
+  __shared__ const uint8_t* sbase[kMaxFusedK];
+  __shared__ float swgt[kMaxFusedK];
+  __shared__ int swait[kMaxFusedK], shost[kMaxFusedK], sslot[kMaxFusedK], sorder[kMaxFusedK];
+  __shared__ uint32_t sgen[kMaxFusedK];
+  __shared__ int snseg;
+  __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
+  __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
+  __shared__ __align__(8) uint64_t gbar;                  // gate rows + x landed
   const ExpertArgs& a = f.e;
+  const RouteArgs& ra = f.r;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
   uint8_t* ring = smem;
   uint8_t* xh = smem + (size_t)NS * SB;
@@ -129,22 +176,29 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 4 * NS);  // full[2u] parity at phase B start
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = a.K, d = a.d, ffr = a.ffr;
+  const int K = a.K, d = a.d, ffr = a.ffr, n = ra.n;
   const int G = gridDim.x, b = blockIdx.x;
-  // expert group of this CTA: group r serves routed expert r (phase A rows j and phase B
-  // rows c of that expert)
-  const int r = (int)((long long)b * K / G);
-  const int gb0 = (int)(((long long)r * G + K - 1) / K);
-  const int gb1 = (int)(((long long)(r + 1) * G + K - 1) / K);
-  const int gsz = gb1 - gb0, li = b - gb0;
   const int rowA = 4 * d;                       // bytes of one W1 row + one W3 row
   const int rowB = ffr * 2;                     // bytes of one W2 row (<= 2*SB)
   const long long w2off = 2ll * ffr * d * 2;    // W2 offset in a slot
+  // bar[r] counts per-stage publications of h_r: G CTAs x NS stages per call
+  const unsigned long long bar_target = (f.calls + 1) * (unsigned long long)G * (unsigned long long)NS;
+  // work-claim counters of this call ([A r][B r]); the other parity is zeroed for the next
+  unsigned* ctr = f.ctr + (f.calls & 1) * (2 * kMaxFusedK);
+  // the ring is free until the route is known: it stages the gate rows and x first
+  const uint32_t gate_bytes = (uint32_t)n * (uint32_t)d * 2u;
+  const uint16_t* gsm = reinterpret_cast<const uint16_t*>(ring);
+  float* zpart = reinterpret_cast<float*>(ring + gate_bytes);  // [consumer warp][n] partial logits
+  // x (bf16) lives in xh through phase A; phase B reuses xh for h_r (fp32)
+  const int cw = warp - 1;                      // consumer warp 0 .. 2*NS-1 (warp 0: producer)
+  const int nthr = kWarpsPerStage * NS * 32;
+  const int ctid = threadIdx.x - 32;
 
+  if (f.sts && threadIdx.x == 0) f.sts[kStsHead + b] = globaltimer();
   if (f.ts && threadIdx.x == 0) {
-    f.ts[b * 8 + 0] = globaltimer();
-    f.ts[b * 8 + 6] = 0;
-    f.ts[b * 8 + 7] = 0;
+    f.ts[b * kTsPerCta + 0] = globaltimer();
+    f.ts[b * kTsPerCta + 6] = 0;
+    f.ts[b * kTsPerCta + 7] = 0;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -152,166 +206,242 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       mbar_init(empty + s, 1);
     }
     mbar_init(hbar, 1);
+    mbar_init(&gbar, 1);
     fence_mbar_init();
+    // the gate rows are weights, constant across calls: stream them in before the PDL wait
+    mbar_arrive_expect_tx(&gbar, gate_bytes + 2u * d);
+    bulk_g2s(ring, ra.Wg, gate_bytes, &gbar, policy_evict_last());
   }
-  // The router kernel publishes its route (release) before it completes: acquire it here
-  // instead of waiting for the router grid's completion and memory flush (PDL launch).
-  if (threadIdx.x == 0) {
-    if (a.route_flag) {
-      while (ld_acquire_u64(a.route_flag) != a.seq) {
+  __syncthreads();          // mbarrier inits visible
+  {
+    // Programmatic dependent launch: the previous call's kernel (cache directory,
+    // counters, h) and the caller's x are complete and visible after this wait.
+    griddep_wait();
+    if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 8] = globaltimer();
+    DirState ds;
+    if (cw == 0) ds = dir_load(ra, lane);          // the routing warp's directory loads in flight
+    if (threadIdx.x == 0) bulk_g2s(xh, a.x, 2u * d, &gbar, policy_evict_last());
+    if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
+      f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
+    if (K == 2 && cw >= 0) {  // y accumulates the two experts: zero this CTA's slice
+                              // (published to the other CTAs with this CTA's h releases)
+      const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
+      for (int c = c0 + ctid; c < c1; c += nthr) a.y[c] = 0.f;
+    }
+    mbar_wait(&gbar, 0);
+    if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 9] = globaltimer();
+    unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
+    if (pm && threadIdx.x == 32) pm[0] = clock64();
+    if (cw >= 0 && cw < kWarpsPerStage * NS) {
+      if (pm && threadIdx.x == 32) pm[1] = clock64();
+      // Gate GEMV z = Wg x: consumer warp w covers 16-B chunks [k0, k1) of every row;
+      // a lane loads its x chunk once and applies it to all n gate rows (shared memory
+      // traffic ~ the gate bytes). Per-warp partial sums, reduced in a fixed order.
+      {
+        const int nwc = kWarpsPerStage * NS;
+        const int nch = d >> 3, cpw = (nch + nwc - 1) / nwc;
+        const int k0 = cw * cpw, k1 = min(nch, k0 + cpw);
+        for (int e0 = 0; e0 < n; e0 += 8) {
+          float acc[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+          for (int k = k0 + lane; k < k1; k += 32) {
+            const int4 xq = reinterpret_cast<const int4*>(xh)[k];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (e0 + i < n) {
+                const float2 t = dot8_bf(reinterpret_cast<const int4*>(gsm + (size_t)(e0 + i) * d)[k], xq,
+                                         make_float2(0.f, 0.f));
+                acc[i] += t.x + t.y;
+              }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float v = warp_sum(acc[i]);
+            if (lane == 0 && e0 + i < n) zpart[cw * n + e0 + i] = v;
+          }
+        }
+      }
+      if (pm && threadIdx.x == 32) pm[2] = clock64();
+      named_bar_sync(1, nthr);
+      if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 10] = globaltimer();
+      if (pm && threadIdx.x == 32) pm[3] = clock64();
+      if (cw == 0) {
+        // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects
+        float z = 0.f;
+        if (lane < n)
+          for (int w = 0; w < kWarpsPerStage * NS; ++w) z += zpart[w * n + lane];  // fixed order
+        LaneRoute lr;
+        const bool writer = b == 0;
+        const int nmiss = route_decide(ra, z, ds, writer, rS, rZ, rW, &lr,
+                                       pm ? pm + 4 : nullptr);
+        if (f.ts && lane == 0) f.ts[b * kTsPerCta + 11] = globaltimer();
+        if (pm && lane == 0) pm[7] = clock64();
+        if (lane < K) {
+          sslot[lane] = lr.slot;
+          sgen[lane] = lr.gen;
+          swait[lane] = lr.wait;
+          shost[lane] = lr.host;
+          sbase[lane] = a.pool + (long long)lr.slot * a.slot_bytes;
+          swgt[lane] = lr.w;
+        }
+        // device-computed experts in processing order: resident ones first, then the ones
+        // whose fill may still be in flight (rank order within each)
+        const unsigned dev_ready = __ballot_sync(0xffffffffu, lane < K && !lr.host && !lr.wait);
+        const unsigned dev_wait = __ballot_sync(0xffffffffu, lane < K && !lr.host && lr.wait);
+        const unsigned below = (1u << lane) - 1u;
+        if (lane < K && !lr.host)
+          sorder[lr.wait ? __popc(dev_ready) + __popc(dev_wait & below) : __popc(dev_ready & below)] = lane;
+        if (lane == 0) {
+          snseg = __popc(dev_ready | dev_wait);
+          // miss mailbox entry (host-mapped): payload, system fence, seq (the fetch
+          // thread's trigger)
+          if (writer && nmiss) {
+            __threadfence_system();
+            ra.mail->seq = ra.seq;
+          }
+        }
       }
     }
   }
-  if (!a.route_flag) griddep_wait();
-  __syncthreads();
-  if (f.ts && threadIdx.x == 0) f.ts[b * 8 + 1] = globaltimer();
-  if (threadIdx.x == 0) {
-    const int slot = a.route->slot[r];
-    sslot = slot;
-    sgen = a.route->gen[r];
-    swait = a.route->wait[r];
-    shost = a.route->host[r];
-    sbase = a.pool + (long long)slot * a.slot_bytes;
-    swgt = a.route->w[r];
-  }
-  for (int i = threadIdx.x; i < (d >> 2); i += kThreadsF) {  // x -> fp32 in shared memory
-    const uint2 v = reinterpret_cast<const uint2*>(a.x)[i];
-    reinterpret_cast<float4*>(xh)[i] = make_float4(bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y));
-  }
-  __syncthreads();
-  const uint8_t* base = sbase;
-
-  if (shost) {
-    // ---------------------------------------------------------------- host-computed expert
-    // (MOE_MISS_HOST_COMPUTE): wait for the host's result on the activation stream
-    // and add w_r * o_r over this CTA's share of y; keep the group barrier count in step.
-    if (threadIdx.x == 0) {
-      red_release_add_u64(f.bar + 16 * r, 1ull);
-      const uint32_t want = (uint32_t)a.seq;
-      const unsigned long long t0 = globaltimer();
-      unsigned ns = 256;
-      while (ld_acquire_u32(a.host_flag + r) != want) {
-        __nanosleep(ns);
-        if (ns < 8192) ns <<= 1;
-        if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
-      }
-    }
-    __syncthreads();
-    const int c0 = (int)((long long)d * li / gsz), c1 = (int)((long long)d * (li + 1) / gsz);
-    const float w = swgt;
-    const float* o = a.host_out + (size_t)r * d;
-    for (int c = c0 + (int)threadIdx.x; c < c1; c += kThreadsF) {
-      const float v = w * __ldcg(o + c);
-      if (K == 1) a.y[c] = v;
-      else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
-    }
-    if (b == 0 && threadIdx.x == 0) *a.last_seq = a.seq;
-    griddep_launch_dependents();
-    return;
-  }
+  __syncthreads();          // route in shared memory; gate staging area free
+  griddep_launch_dependents();
+  if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
+  const int nseg = snseg;
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      if (swait) wait_ready(a.ready, sslot, sgen);  // fill of this slot still in flight
-      unsigned* ctrA = f.ctr + r;
-      unsigned* ctrB = f.ctr + kMaxK + r;
+      for (int r = 0; r < K; ++r)  // host-computed experts have no h: publish them at once
+        if (shost[r]) red_release_add_u64(f.bar + 16 * r, (unsigned long long)NS);
       uint32_t use = 0;                               // per-stage use-count parity bits
       auto acquire = [&](int s) {                     // wait until stage s is free
         mbar_wait(empty + s, ((use >> s) & 1) ^ 1);
         use ^= 1u << s;
       };
       int t = 0;
-      auto issue_a = [&](int j) {
-        const int s = t % NS;
-        acquire(s);
-        const uint8_t* w1 = base + (long long)j * d * 2;
-        const uint8_t* w3 = w1 + (long long)ffr * d * 2;
-        meta[s] = j;
-        mbar_arrive_expect_tx(full + s, (uint32_t)rowA);
-        bulk_g2s(ring + (size_t)s * SB, w1, 2u * d, full + s, pol);
-        bulk_g2s(ring + (size_t)s * SB + 2 * d, w3, 2u * d, full + s, pol);
-        ++t;
+      auto marker_a = [&](int m) {                    // one marker into each of the NS stages
+        for (int k = 0; k < NS; ++k, ++t) {
+          const int s = t % NS;
+          acquire(s);
+          meta[s] = m;
+          mbar_arrive(full + s);
+        }
       };
-      // phase A: static block, then tail claims (two claims in flight hide the atomic latency)
-      const RowSched sa = make_sched(ffr, li, gsz);
-      unsigned c1 = atomicAdd(ctrA, (unsigned)kChunkA);
-      for (int j = sa.s0; j < sa.s1; ++j) issue_a(j);
-      unsigned c2 = atomicAdd(ctrA, (unsigned)kChunkA);
-      while (sa.tail0 + (int)c1 < ffr) {
-        const int j0 = sa.tail0 + (int)c1, j1 = min(j0 + kChunkA, ffr);
-        c1 = c2;
-        if (sa.tail0 + (int)c1 < ffr) c2 = atomicAdd(ctrA, (unsigned)kChunkA);
-        for (int j = j0; j < j1; ++j) issue_a(j);
+      // phase A: per segment, static block then tail claims (two claims in flight hide the
+      // atomic latency)
+      const RowSched sa = make_sched(ffr, b, G);
+      for (int si = 0; si < nseg; ++si) {
+        const int r = sorder[si];
+        const uint8_t* base = sbase[r];
+        if (swait[r]) wait_ready(a.ready, sslot[r], sgen[r]);  // fill of this slot still in flight
+        unsigned* cA = ctr + r;
+        auto issue_a = [&](int j) {
+          const int s = t % NS;
+          acquire(s);
+          const uint8_t* w1 = base + (long long)j * d * 2;
+          const uint8_t* w3 = w1 + (long long)ffr * d * 2;
+          meta[s] = (r << 24) | j;
+          mbar_arrive_expect_tx(full + s, (uint32_t)rowA);
+          bulk_g2s(ring + (size_t)s * SB, w1, 2u * d, full + s, pol);
+          bulk_g2s(ring + (size_t)s * SB + 2 * d, w3, 2u * d, full + s, pol);
+          ++t;
+        };
+        unsigned c1 = atomicAdd(cA, (unsigned)kChunkA);
+        for (int j = sa.s0; j < sa.s1; ++j) issue_a(j);
+        unsigned c2 = atomicAdd(cA, (unsigned)kChunkA);
+        while (sa.tail0 + (int)c1 < ffr) {
+          const int j0 = sa.tail0 + (int)c1, j1 = min(j0 + kChunkA, ffr);
+          c1 = c2;
+          if (sa.tail0 + (int)c1 < ffr) c2 = atomicAdd(cA, (unsigned)kChunkA);
+          for (int j = j0; j < j1; ++j) issue_a(j);
+        }
+        marker_a(kSegA - r);  // every stage publishes its rows of h_r
       }
-      for (int k = 0; k < NS; ++k, ++t) {  // one end-of-phase marker per stage
-        const int s = t % NS;
-        acquire(s);
-        meta[s] = -1;
-        mbar_arrive(full + s);
-      }
+      marker_a(kEnd);
       // phase B: whole W2 rows into super-stages (2u, 2u+1); W2 does not depend on h, so
-      // these loads stream while the consumers finish phase A and cross the barrier
+      // these loads stream while the consumers finish phase A and load h
       int tb = 0;
-      auto issue_b = [&](int c) {
-        const int u = tb % NSB, s = 2 * u;
-        acquire(s);
-        meta[s] = c;
-        mbar_arrive_expect_tx(full + s, (uint32_t)rowB);
-        bulk_g2s(ring + (size_t)s * SB, base + w2off + (long long)c * rowB, (uint32_t)rowB, full + s, pol);
-        ++tb;
+      auto marker_b = [&](int m) {
+        for (int k = 0; k < NSB; ++k, ++tb) {
+          const int s = 2 * (tb % NSB);
+          acquire(s);
+          meta[s] = m;
+          mbar_arrive(full + s);
+        }
       };
-      const RowSched sbk = make_sched(d, li, gsz);
-      c1 = atomicAdd(ctrB, (unsigned)kChunkB);
-      for (int c = sbk.s0; c < sbk.s1; ++c) issue_b(c);
-      c2 = atomicAdd(ctrB, (unsigned)kChunkB);
-      while (sbk.tail0 + (int)c1 < d) {
-        const int r0 = sbk.tail0 + (int)c1, r1 = min(r0 + kChunkB, d);
-        c1 = c2;
-        if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(ctrB, (unsigned)kChunkB);
-        for (int c = r0; c < r1; ++c) issue_b(c);
+      const RowSched sbk = make_sched(d, b, G);
+      for (int si = 0; si < nseg; ++si) {
+        const int r = sorder[si];
+        const uint8_t* w2 = sbase[r] + w2off;
+        unsigned* cB = ctr + kMaxFusedK + r;
+        auto issue_b = [&](int c) {
+          const int s = 2 * (tb % NSB);
+          acquire(s);
+          meta[s] = c;
+          mbar_arrive_expect_tx(full + s, (uint32_t)rowB);
+          bulk_g2s(ring + (size_t)s * SB, w2 + (long long)c * rowB, (uint32_t)rowB, full + s, pol);
+          ++tb;
+        };
+        if (si > 0) marker_b(kSegB);
+        unsigned c1 = atomicAdd(cB, (unsigned)kChunkB);
+        for (int c = sbk.s0; c < sbk.s1; ++c) issue_b(c);
+        unsigned c2 = atomicAdd(cB, (unsigned)kChunkB);
+        while (sbk.tail0 + (int)c1 < d) {
+          const int r0 = sbk.tail0 + (int)c1, r1 = min(r0 + kChunkB, d);
+          c1 = c2;
+          if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(cB, (unsigned)kChunkB);
+          for (int c = r0; c < r1; ++c) issue_b(c);
+        }
       }
-      for (int k = 0; k < NSB; ++k, ++tb) {
-        const int s = 2 * (tb % NSB);
-        acquire(s);
-        meta[s] = -1;
-        mbar_arrive(full + s);
+      marker_b(kEnd);
+      // publish the call's progress to the host fetch thread (PCIe write overlaps the tail);
+      // the system fence orders this call's mailbox entry (written by the routing warp
+      // before the CTA barrier) before it
+      if (b == 0) {
+        __threadfence_system();
+        *a.last_seq = a.seq;
       }
-      // publish the call's progress to the host fetch thread (PCIe write overlaps the tail)
-      if (b == 0) *a.last_seq = a.seq;
     }
     return;
   }
 
   // -------------------------------------------------------------------- consumers
-  const int cw = warp - 1;                 // consumer warp 0 .. 2*NS-1
   if (cw >= kWarpsPerStage * NS) return;
-  const int nthr = kWarpsPerStage * NS * 32;
   const int sA = cw >> 1, half = cw & 1;   // phase A: stage and half of the row
-  float* hglob = a.h + (long long)r * ffr;
   uint32_t ph = 0;                         // parity of the barrier this warp waits on
   {
     const int nchA = d >> 3;               // 16-B chunks per W1 (or W3) row
     const int c0 = half * (nchA >> 1), c1 = half ? nchA : (nchA >> 1);
-    const float4* xv = reinterpret_cast<const float4*>(xh);
+    const int4* xq = reinterpret_cast<const int4*>(xh);  // x, bf16
     const int4* w1 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB);
     const int4* w3 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB + 2 * d);
     bool first = true;
     while (true) {
       mbar_wait(full + sA, ph);
       ph ^= 1;
-      const int j = meta[sA];
-      if (j < 0) break;
-      if (f.ts && first && cw == 0 && lane == 0) f.ts[b * 8 + 2] = globaltimer();
+      const int m = meta[sA];
+      if (m < 0) {
+        if (m == kEnd) break;
+        // end of segment r in this stage: its h writer (half 0, lane 0) wrote every row of
+        // h_r this stage produced; publish them (release at gpu scope covers its own stores)
+        named_bar_sync(2 + sA, 64);        // both halves read meta before the stage is reused
+        if (half == 0 && lane == 0) {
+          mbar_arrive(empty + sA);
+          red_release_add_u64(f.bar + 16 * (kSegA - m), 1ull);
+        }
+        continue;
+      }
+      const int r = m >> 24, j = m & 0xFFFFFF;
+      if (f.ts && first && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 2] = globaltimer();
       first = false;
-      const unsigned long long tp0 = (f.ts && cw == 0) ? globaltimer() : 0ull;
       float2 g = make_float2(0.f, 0.f), u = make_float2(0.f, 0.f);
 #pragma unroll 4
       for (int c = c0 + lane; c < c1; c += 32) {
-        const float4 xa = xv[2 * c], xb = xv[2 * c + 1];
-        g = dot8(w1[c], xa, xb, g);
-        u = dot8(w3[c], xa, xb, u);
+        const int4 xc = xq[c];
+        g = dot8_bf(w1[c], xc, g);
+        u = dot8_bf(w3[c], xc, u);
       }
       const float gs = warp_sum(g.x + g.y);
       const float us = warp_sum(u.x + u.y);
@@ -321,82 +451,109 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       }
       named_bar_sync(2 + sA, 64);          // both halves of stage sA done (reads + partials)
       if (half == 0 && lane == 0) {
-        mbar_arrive(empty + sA);
         const float gg = part[4 * sA + 0] + part[4 * sA + 2];   // fixed order: half 0 + half 1
         const float uu = part[4 * sA + 1] + part[4 * sA + 3];
-        hglob[h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
-        if (f.ts && cw == 0) f.ts[b * 8 + 6] += globaltimer() - tp0;
+        mbar_arrive(empty + sA);           // (partials read first: half 1 rewrites them next row)
+        a.h[(long long)r * ffr + h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
       }
     }
     named_bar_sync(2 + sA, 64);
     if (half == 0 && lane == 0) mbar_arrive(empty + sA);  // release the end marker's stage
     if (half == 0 && lane == 0 && (sA & 1) == 0) parB[sA >> 1] = ph;  // full[sA] parity for phase B
   }
-  named_bar_sync(1, nthr);
-  if (f.ts && cw == 0 && lane == 0) f.ts[b * 8 + 3] = globaltimer();
-  if (f.ts && cw == 0 && lane == 0) f.ts[b * 8 + 7] = 0;
-  // Per-expert barrier: all h_r rows (written by the gsz CTAs of this group) are visible
-  // before any of them is read. Release-RED arrival, acquire spin (PTX memory model:
-  // bar.sync + release at gpu scope publishes the whole CTA's writes).
-  if (cw == 0 && lane == 0) {
-    unsigned long long* bar = f.bar + 16 * r;   // one 128-B line per expert group
-    const unsigned long long target = (f.calls + 1) * (unsigned long long)gsz;
-    if (f.barmode == 1) {          // experiment: fence + relaxed atomic, relaxed spin + fence
-      __threadfence();
-      atomicAdd(bar, 1ull);
-      while (*((volatile unsigned long long*)bar) < target) __nanosleep(40);
-      __threadfence();
-    } else if (f.barmode == 2) {   // experiment: release RED, acquire spin without backoff
-      red_release_add_u64(bar, 1ull);
-      while (ld_acquire_u64(bar) < target) {
+  if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 3] = globaltimer();
+  // h_r -> shared memory (xh) before phase-B segment r: every consumer is done with xh,
+  // every stage of every CTA has published its rows of h_r (acquire), then ONE bulk copy
+  // (the async proxy reads global memory written through the generic proxy by other CTAs:
+  // fence the proxies first).
+  uint32_t hph = 0;
+  auto load_h = [&](int r) {
+    named_bar_sync(1, nthr);
+    if (cw == 0 && lane == 0) {
+      const unsigned long long* bar = f.bar + 16 * r;
+      if (ld_acquire_u64(bar) < bar_target) {
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_u64(bar) < bar_target) {
+          __nanosleep(32);
+          if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+        }
       }
-    } else {
-      red_release_add_u64(bar, 1ull);
-      while (ld_acquire_u64(bar) < target) __nanosleep(40);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      mbar_arrive_expect_tx(hbar, (uint32_t)ffr * 4u);
+      bulk_g2s(xh, a.h + (long long)r * ffr, (uint32_t)ffr * 4u, hbar, policy_evict_first());
     }
-    if (f.ts) f.ts[b * 8 + 4] = globaltimer();
-    // h_r -> shared memory with one bulk copy (the async proxy reads global memory written
-    // through the generic proxy by other CTAs: fence the proxies first)
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    mbar_arrive_expect_tx(hbar, (uint32_t)ffr * 4u);
-    bulk_g2s(xh, hglob, (uint32_t)ffr * 4u, hbar, policy_evict_first());
-  }
-  mbar_wait(hbar, 0);
+    mbar_wait(hbar, hph);
+    hph ^= 1;
+  };
   {
     const int u = cw >> 2, q = cw & 3;     // super-stage and quarter of the W2 row
-    if (u >= NSB) return;                  // (NS odd: the last stage's warps sit out phase B)
+    const bool active = u < NSB;           // (NS odd: the last stage's warps sit out phase B)
     const int s = 2 * u;
-    ph = parB[u];
     const int nck = rowB >> 4;
     const int k0 = (nck * q) >> 2, k1 = (nck * (q + 1)) >> 2;
     const float4* hp0 = reinterpret_cast<const float4*>(xh);   // h[8c .. 8c+3]
     const float4* hp1 = hp0 + (ffr >> 3);                      // h[8c+4 .. 8c+7]
     const int4* wv = reinterpret_cast<const int4*>(ring + (size_t)s * SB);
-    const float w = swgt;
-    while (true) {
-      mbar_wait(full + s, ph);
-      ph ^= 1;
-      const int c = meta[s];
-      if (c < 0) break;
-      const unsigned long long tp0 = (f.ts && cw == 0) ? globaltimer() : 0ull;
-      float2 acc = make_float2(0.f, 0.f);
+    for (int si = 0; si < nseg; ++si) {
+      const int r = sorder[si];
+      const float w = swgt[r];
+      load_h(r);
+      if (si == 0 && active) ph = parB[u];  // written before load_h's barrier
+      if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + (si == 0 ? 4 : 6)] = globaltimer();
+      if (!active) continue;
+      while (true) {
+        mbar_wait(full + s, ph);
+        ph ^= 1;
+        const int c = meta[s];
+        if (c < 0) {                       // kSegB (next expert) or kEnd
+          named_bar_sync(2 + u, 128);
+          if (q == 0 && lane == 0) mbar_arrive(empty + s);
+          break;
+        }
+        float2 acc = make_float2(0.f, 0.f);
 #pragma unroll 4
-      for (int cc = k0 + lane; cc < k1; cc += 32) acc = dot8(wv[cc], hp0[cc], hp1[cc], acc);
-      const float sum = warp_sum(acc.x + acc.y);
-      if (lane == 0) part[4 * u + q] = sum;
-      named_bar_sync(2 + u, 128);          // the 4 quarters of this row are done
-      if (q == 0 && lane == 0) {
-        mbar_arrive(empty + s);
-        const float o = ((part[4 * u] + part[4 * u + 1]) + part[4 * u + 2]) + part[4 * u + 3];
-        if (K == 1) a.y[c] = w * o;
-        else red_add_f32(a.y + c, w * o);  // K == 2: 0 + a + b is order-independent
-        if (f.ts && cw == 0) f.ts[b * 8 + 7] += globaltimer() - tp0;
+        for (int cc = k0 + lane; cc < k1; cc += 32) acc = dot8(wv[cc], hp0[cc], hp1[cc], acc);
+        const float sum = warp_sum(acc.x + acc.y);
+        if (lane == 0) part[4 * u + q] = sum;
+        named_bar_sync(2 + u, 128);        // the 4 quarters of this row are done
+        if (q == 0 && lane == 0) {
+          const float o = ((part[4 * u] + part[4 * u + 1]) + part[4 * u + 2]) + part[4 * u + 3];
+          mbar_arrive(empty + s);          // (partials read first: the next row rewrites them)
+          if (K == 1) a.y[c] = w * o;
+          else red_add_f32(a.y + c, w * o);  // K == 2: 0 + a + b is order-independent
+        }
       }
-      named_bar_sync(2 + u, 128);          // partials consumed before they are overwritten
     }
   }
-  if (f.ts && cw == 0 && lane == 0) f.ts[b * 8 + 5] = globaltimer();
-  griddep_launch_dependents();
+  // host-computed experts (MOE_MISS_HOST_COMPUTE): wait for the host's result on the
+  // activation stream and add w_r * o_r over this CTA's share of y
+  for (int r = 0; r < K; ++r) {
+    if (!shost[r]) continue;
+    if (cw == 0 && lane == 0) {
+      // every CTA zeroed its slice of y before publishing on bar[r] (release)
+      while (ld_acquire_u64(f.bar + 16 * r) < bar_target) {
+      }
+      const uint32_t want = (uint32_t)a.seq;
+      const unsigned long long t0 = globaltimer();
+      unsigned ns = 256;
+      while (ld_acquire_u32(a.host_flag + r) != want) {
+        __nanosleep(ns);
+        if (ns < 8192) ns <<= 1;
+        if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+      }
+    }
+    named_bar_sync(1, nthr);
+    const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
+    const float w = swgt[r];
+    const float* o = a.host_out + (size_t)r * d;
+    for (int c = c0 + ctid; c < c1; c += nthr) {
+      const float v = w * __ldcg(o + c);
+      if (K == 1) a.y[c] = v;
+      else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
+    }
+  }
+  if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 5] = globaltimer();
+  if (f.sts && cw == 0 && lane == 0) f.sts[kStsHead + G + b] = globaltimer();
 }
 
 }  // namespace
@@ -409,28 +566,29 @@ cudaError_t preload_fused_kernels() {
                               kFusedMaxDynSmem);
 }
 
-bool plan_fused(int d, int ffr, int K, int grid, FusedPlan* p) {
+bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   if (K > 2 || grid < K) return false;          // deterministic combine needs K <= 2
   const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
   if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
-  const int xh = ((max(4 * d, ffr * 4) + 127) / 128) * 128;   // x (fp32) | one expert's h (fp32)
+  const int xh = ((max(2 * d, ffr * 4) + 127) / 128) * 128;   // x (bf16) | one expert's h (fp32)
   const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + 64;
   int NS = (kFusedMaxDynSmem - xh - tail) / SB;
   if (NS > kMaxNS) NS = kMaxNS;
   NS &= ~1;                                      // stages pair into super-stages in phase B
   if (NS < 4) return false;
+  // the gate rows and x are staged in the (still empty) ring before the route is known
+  const long long gate = 2ll * n * d;                                   // staged in the ring
+  const long long zp = 4ll * kWarpsPerStage * kMaxNS * MOE_MAX_EXPERTS;  // partial logits
+  if (n > MOE_MAX_EXPERTS || gate + zp > (long long)NS * SB || gate + 2ll * d >= (1ll << 20)) return false;
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;
-  p->ypart_bytes = 0;
   p->smem = (size_t)NS * SB + xh + tail;
   p->threads = kThreadsF;
-  p->partB = 2 * ffr;
-  p->copiesB = 1;
   return p->smem <= (size_t)kFusedMaxDynSmem;
 }
 
-cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl) {
+cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl, bool coop) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(p.threads);
@@ -438,9 +596,11 @@ cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int na = 0;
-  at[na].id = cudaLaunchAttributeCooperative;
-  at[na].val.cooperative = 1;
-  ++na;
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
   if (pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;

@@ -14,6 +14,8 @@ namespace moe {
 
 constexpr int kMaxK = MOE_MAX_EXPERTS;  // K <= n <= 32
 constexpr int kMailRing = 1024;         // miss-notification mailbox entries (host-mapped)
+constexpr int kStsRing = 64;            // debug step-timestamp records (MOE_DEBUG_TS)
+constexpr int kStsHead = 8;             // router marks per record
 
 // Per-layer device counters, same order as moe_layer_stats.
 struct DevStats {
@@ -69,9 +71,7 @@ struct RouteArgs {
   uint16_t* xmail;     // device alias of the host-mapped x slot of this call (host compute)
   unsigned long long seq;
   long long slot_bytes;
-  float* y_zero;       // if non-null: zero y[0..d) (the fused expert kernel accumulates into it)
-  unsigned long long* route_flag;  // release-published = seq once the route record is complete
-  unsigned* sched_zero;  // if non-null: zero the fused kernel's 2*kMaxK work-claim counters
+  unsigned long long* sts;  // debug (MOE_DEBUG_TS): this call's step-timestamp record, or nullptr
 };
 
 struct ExpertArgs {
@@ -85,7 +85,6 @@ struct ExpertArgs {
   const uint32_t* ready;
   volatile unsigned long long* last_seq;  // host-mapped progress word, written at the end
   unsigned long long seq;                 // this call's sequence number
-  const unsigned long long* route_flag;   // == seq once the router kernel published the route
   const float* host_out;                  // [kMaxK][d] host-computed expert outputs (device copy)
   const uint32_t* host_flag;              // [kMaxK] == (uint32_t)seq once host_out[r] landed
 };
@@ -93,25 +92,24 @@ struct ExpertArgs {
 // Fused persistent expert kernel (expert_fused.cu).
 constexpr int kFusedMaxDynSmem = 232448 - 1024;  // 227 KB opt-in minus static shared memory
 struct FusedArgs {
+  RouteArgs r;                    // routing inputs (every CTA takes the decision; CTA 0 writes it)
   ExpertArgs e;
-  unsigned long long* bar;        // per-expert group-barrier counters [K] (monotonic across calls)
+  unsigned long long* bar;        // per-expert h publication counters [K] (monotonic across calls)
   unsigned long long calls;       // number of earlier fused launches on this context
   unsigned* ctr;                  // work-claim counters [2][kMaxK] (phase A rows, phase B rows), zeroed per call
   int NS, SB;                     // ring stages / stage bytes
-  int xh_bytes, ypart_bytes;
-  int partB;                      // bytes per W2-row part (<= SB, multiple of 16)
-  int copiesB;                    // bulk copies per phase B part (1 or 2)
-  int barmode;                    // phase barrier variant (experiments; 0 = default)
+  int xh_bytes;
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
-  unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_KERNEL=1) or nullptr
+  unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
+  unsigned long long* sts;        // this call's step record [kStsHead + 2*grid] (MOE_DEBUG_TS=1) or nullptr
 };
 struct FusedPlan {
-  int SB, NS, xh_bytes, ypart_bytes, threads, partB, copiesB;
+  int SB, NS, xh_bytes, threads;
   size_t smem;
 };
-bool plan_fused(int d, int ffr, int K, int grid, FusedPlan* p);
+bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);
 
-cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl);
+cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl, bool coop);
 cudaError_t preload_fused_kernels();
 
 cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl);

@@ -173,8 +173,6 @@ struct moe_ctx {
   int fused_grid = 0;
   unsigned long long* d_bar = nullptr;
   unsigned* d_ctr = nullptr;  // fused kernel work-claim counters
-  unsigned long long* d_route_flag = nullptr;  // router -> expert kernel handoff word
-  int barmode = 0;
   // MOE_MISS_HOST_COMPUTE: x ring (host-mapped), host outputs, activation stream
   int miss_mode = MOE_MISS_FETCH;
   HostExpert* host = nullptr;
@@ -199,7 +197,9 @@ struct moe_ctx {
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
-  unsigned long long* d_ts = nullptr;  // per-CTA phase timestamps (MOE_DEBUG_KERNEL=1)
+  unsigned long long* d_ts = nullptr;  // per-CTA phase timestamps (MOE_DEBUG_TS=1)
+  bool coop = true;                    // cooperative launch of the fused expert kernel
+  unsigned long long* d_sts = nullptr; // per-call step timestamps, ring of kStsRing (MOE_DEBUG_TS=1)
 };
 
 namespace {
@@ -392,8 +392,19 @@ MOE_API int moe_debug_tc_gemm(const void* A, const void* B, float* C, int M, int
 MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
   if (!c || !c->d_ts) return 0;
   cudaDeviceSynchronize();
-  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * 8 * c->fused_grid, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * 40 * c->fused_grid, cudaMemcpyDeviceToHost);
   return c->fused_grid;
+}
+
+// Debug only (not in moe.h): the per-call step timestamps (globaltimer ns) of the last
+// kStsRing calls, [kStsRing][kStsHead + 2*grid] = router marks (after its PDL wait, publish,
+// gate GEMV done, softmax done, before the release fence), expert CTA starts, expert CTA ends; slot = seq % kStsRing. Returns the record stride or 0.
+MOE_API int moe_debug_step_ts(moe_ctx* c, unsigned long long* out) {
+  if (!c || !c->d_sts) return 0;
+  cudaDeviceSynchronize();
+  const int stride = kStsHead + 2 * c->fused_grid;
+  cudaMemcpy(out, c->d_sts, sizeof(unsigned long long) * kStsRing * stride, cudaMemcpyDeviceToHost);
+  return stride;
 }
 
 // Debug only (not in moe.h): host pointer to the mapped kernel progress words, or NULL.
@@ -515,8 +526,6 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * 2 * kMaxK));
-  INIT_TRY(cudaMalloc(&c->d_route_flag, 128));
-  INIT_TRY(cudaMemset(c->d_route_flag, 0, 128));
   INIT_TRY(cudaHostAlloc((void**)&c->h_xring, sizeof(uint16_t) * (size_t)d * kMailRing, cudaHostAllocMapped));
   INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_xring, c->h_xring, 0));
   INIT_TRY(cudaHostAlloc((void**)&c->h_hout, sizeof(float) * (size_t)d * kMaxK, cudaHostAllocDefault));
@@ -529,31 +538,24 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
     const char* path = getenv("MOE_EXPERT_PATH");
     const char* pdl = getenv("MOE_PDL");
     c->pdl = !(pdl && pdl[0] == '0');
+    const char* coop = getenv("MOE_COOP");
+    c->coop = !(coop && coop[0] == '0');
     c->fused_grid = c->num_sms;
-    c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, K, c->fused_grid, &c->plan);
-    if (c->fused) {  // tuning knobs (experiments): W2-row part bytes / bulk copies per part
-      const char* pb = getenv("MOE_FB_PART");
-      const char* cb = getenv("MOE_FB_COPIES");
-      if (pb) {
-        const int v = atoi(pb);
-        if (v >= 16 && v % 16 == 0 && v <= c->plan.SB && (2 * c->ffr + v - 1) / v <= 2) c->plan.partB = v;
-      }
-      if (cb) c->plan.copiesB = atoi(cb) == 2 ? 2 : 1;
-      const char* bm = getenv("MOE_BARMODE");
-      if (bm) c->barmode = atoi(bm);
-    }
+    c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, n, K, c->fused_grid, &c->plan);
     if (getenv("MOE_DEBUG_KERNEL")) {  // progress words in host-mapped memory (slow: PCIe atomics)
       INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
       memset(c->h_dbg, 0, 64);
       INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_dbg, c->h_dbg, 0));
     }
     if (getenv("MOE_DEBUG_TS")) {      // per-CTA phase timestamps in device memory (cheap)
-      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 8 * c->fused_grid));
-      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 8 * c->fused_grid));
+      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 40 * c->fused_grid));
+      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 40 * c->fused_grid));
+      INIT_TRY(cudaMalloc(&c->d_sts, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
+      INIT_TRY(cudaMemset(c->d_sts, 0, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
     }
     if (getenv("MOE_DEBUG_KERNEL") || getenv("MOE_DEBUG_TS")) {
-      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d xh=%d ypart=%d smem=%zu grid=%d\n", (int)c->fused,
-              c->plan.NS, c->plan.SB, c->plan.xh_bytes, c->plan.ypart_bytes, c->plan.smem, c->fused_grid);
+      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d xh=%d smem=%zu grid=%d\n", (int)c->fused, c->plan.NS,
+              c->plan.SB, c->plan.xh_bytes, c->plan.smem, c->fused_grid);
   }
   }
   {
@@ -606,7 +608,6 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_bar);
   cudaFree(c->d_ctr);
-  cudaFree(c->d_route_flag);
   cudaFree(c->d_hout);
   cudaFree(c->d_hflag);
   cudaFree(c->d_pfscratch);
@@ -623,6 +624,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   delete c->host;
   c->host = nullptr;
   cudaFree(c->d_ts);
+  cudaFree(c->d_sts);
   if (c->h_mail) cudaFreeHost(c->h_mail);
   if (c->h_last) cudaFreeHost((void*)c->h_last);
   for (void* p : c->registered) cudaHostUnregister(p);
@@ -793,10 +795,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.trace_cap = c->trace_cap;
   ra.token = c->tokens[layer];
   ra.mail = c->d_mail + (seq % kMailRing);
-  ra.y_zero = (c->fused && c->K == 2) ? y : nullptr;  // the fused kernel reduces the K experts into y
-  ra.sched_zero = c->fused ? c->d_ctr : nullptr;
-  ra.route_flag = c->fused ? c->d_route_flag : nullptr;
   ra.seq = seq;
+  ra.sts = c->d_sts ? c->d_sts + (seq % kStsRing) * (kStsHead + 2 * c->fused_grid) : nullptr;
   ra.slot_bytes = c->slot_bytes;
 
   ExpertArgs ea;
@@ -810,19 +810,15 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ea.ready = c->d_ready;
   ea.last_seq = c->d_last;
   ea.seq = seq;
-  ea.route_flag = c->fused ? c->d_route_flag : nullptr;
   ea.host_out = c->d_hout;
   ea.host_flag = c->d_hflag;
 
   ProfEv pe;
-  prof_begin(c, 0, s, &pe);
-  CUDA_TRY(launch_route_probe(ra, s, c->pdl));
-  prof_end(c, s, &pe);
-  c->issued.store(seq, std::memory_order_release);  // the fetch thread may now wait for it
-  c->tokens[layer] += 1;
-  c->trace_count += c->K;
   if (c->fused) {
+    // ONE kernel per call: every CTA takes the routing decision itself (CTA 0 writes the
+    // directory, trace, counters and mailbox), then streams the experts
     FusedArgs fa;
+    fa.r = ra;
     fa.e = ea;
     fa.bar = c->d_bar;
     fa.calls = c->fused_calls;
@@ -830,23 +826,25 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.NS = c->plan.NS;
     fa.SB = c->plan.SB;
     fa.xh_bytes = c->plan.xh_bytes;
-    fa.ypart_bytes = c->plan.ypart_bytes;
-    fa.partB = c->plan.partB;
-    fa.copiesB = c->plan.copiesB;
-    fa.barmode = c->barmode;
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
+    fa.sts = ra.sts;
     prof_begin(c, 1, s, &pe);
-    cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl);
-    if (e != cudaSuccess && c->pdl) {  // cooperative + PDL not accepted: retry without PDL
+    cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl, c->coop);
+    if (e != cudaSuccess && c->pdl) {  // PDL not accepted: retry without it
       cudaGetLastError();
       c->pdl = false;
-      e = launch_expert_fused(fa, c->plan, c->fused_grid, s, false);
+      e = launch_expert_fused(fa, c->plan, c->fused_grid, s, false, c->coop);
     }
     prof_end(c, s, &pe);
     if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("expert_fused launch: ") + cudaGetErrorString(e));
     c->fused_calls += 1;
+    c->issued.store(seq, std::memory_order_release);  // the fetch thread may now wait for it
   } else {
+    prof_begin(c, 0, s, &pe);
+    CUDA_TRY(launch_route_probe(ra, s, c->pdl));
+    prof_end(c, s, &pe);
+    c->issued.store(seq, std::memory_order_release);
     prof_begin(c, 1, s, &pe);
     launch_expert_gateup(ea, s, c->num_sms);
     prof_end(c, s, &pe);
@@ -855,6 +853,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     prof_end(c, s, &pe);
     CUDA_TRY(cudaGetLastError());
   }
+  c->tokens[layer] += 1;
+  c->trace_count += c->K;
   if (c->P > 1) {
     prof_begin(c, 3, s, &pe);
     ncclResult_t r = g_nccl.AllReduce(y, y, (size_t)c->d, ncclFloat32, ncclSum, c->comm, s);
