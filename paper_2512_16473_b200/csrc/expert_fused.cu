@@ -162,9 +162,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ int snseg;
   __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
   __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
-  __shared__ __align__(8) uint64_t gbar;                  // gate rows + x landed
+  __shared__ __align__(8) uint64_t gbar, xbar;            // gate rows landed / x landed
+  __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
-  const RouteArgs& ra = f.r;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
   uint8_t* ring = smem;
   uint8_t* xh = smem + (size_t)NS * SB;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 4 * NS);  // full[2u] parity at phase B start
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = a.K, d = a.d, ffr = a.ffr, n = ra.n;
+  const int K = a.K, d = a.d, ffr = a.ffr, n = f.r.n;
   const int G = gridDim.x, b = blockIdx.x;
   const int rowA = 4 * d;                       // bytes of one W1 row + one W3 row
   const int rowB = ffr * 2;                     // bytes of one W2 row (<= 2*SB)
@@ -207,12 +207,29 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
     mbar_init(hbar, 1);
     mbar_init(&gbar, 1);
+    mbar_init(&xbar, 1);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
-    mbar_arrive_expect_tx(&gbar, gate_bytes + 2u * d);
-    bulk_g2s(ring, ra.Wg, gate_bytes, &gbar, policy_evict_last());
+    mbar_arrive_expect_tx(&gbar, gate_bytes);
+    bulk_g2s(ring, f.r.Wg, gate_bytes, &gbar, policy_evict_last());
   }
-  __syncthreads();          // mbarrier inits visible
+  if (threadIdx.x == 32) ra = f.r;  // kernel parameters -> shared memory before the PDL wait
+  __syncthreads();          // mbarrier inits and routing arguments visible
+  // Gate GEMV z = Wg x: consumer warp w covers 16-B chunks [k0, k1) of every row, a
+  // lane one x chunk against all n gate rows. The first chunk of the first 8 rows is held in
+  // registers, loaded before the PDL wait (the gate is constant across calls).
+  const int nwc = kWarpsPerStage * NS;
+  const int nch = d >> 3, cpw = (nch + nwc - 1) / nwc;
+  const int gk0 = cw * cpw, gk1 = min(nch, gk0 + cpw);
+  int4 greg[8];
+  if (cw >= 0 && cw < nwc) {
+    mbar_wait(&gbar, 0);
+    if (gk0 + lane < gk1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < n) greg[i] = reinterpret_cast<const int4*>(gsm + (size_t)i * d)[gk0 + lane];
+    }
+  }
   {
     // Programmatic dependent launch: the previous call's kernel (cache directory,
     // counters, h) and the caller's x are complete and visible after this wait.
@@ -220,7 +237,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 8] = globaltimer();
     DirState ds;
     if (cw == 0) ds = dir_load(ra, lane);          // the routing warp's directory loads in flight
-    if (threadIdx.x == 0) bulk_g2s(xh, a.x, 2u * d, &gbar, policy_evict_last());
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&xbar, 2u * d);
+      bulk_g2s(xh, a.x, 2u * d, &xbar, policy_evict_last());
+    }
     if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
       f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
     if (K == 2 && cw >= 0) {  // y accumulates the two experts: zero this CTA's slice
@@ -228,30 +248,26 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
       for (int c = c0 + ctid; c < c1; c += nthr) a.y[c] = 0.f;
     }
-    mbar_wait(&gbar, 0);
+    mbar_wait(&xbar, 0);
     if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 9] = globaltimer();
     unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
     if (pm && threadIdx.x == 32) pm[0] = clock64();
     if (cw >= 0 && cw < kWarpsPerStage * NS) {
       if (pm && threadIdx.x == 32) pm[1] = clock64();
-      // Gate GEMV z = Wg x: consumer warp w covers 16-B chunks [k0, k1) of every row;
-      // a lane loads its x chunk once and applies it to all n gate rows (shared memory
-      // traffic ~ the gate bytes). Per-warp partial sums, reduced in a fixed order.
+      // gate GEMV: per-warp partial sums, reduced in a fixed order by the routing warp
       {
-        const int nwc = kWarpsPerStage * NS;
-        const int nch = d >> 3, cpw = (nch + nwc - 1) / nwc;
-        const int k0 = cw * cpw, k1 = min(nch, k0 + cpw);
         for (int e0 = 0; e0 < n; e0 += 8) {
           float acc[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-          for (int k = k0 + lane; k < k1; k += 32) {
+          for (int k = gk0 + lane; k < gk1; k += 32) {
             const int4 xq = reinterpret_cast<const int4*>(xh)[k];
+            const bool inreg = e0 == 0 && k == gk0 + lane;
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               if (e0 + i < n) {
-                const float2 t = dot8_bf(reinterpret_cast<const int4*>(gsm + (size_t)(e0 + i) * d)[k], xq,
-                                         make_float2(0.f, 0.f));
+                const int4 gq = inreg ? greg[i] : reinterpret_cast<const int4*>(gsm + (size_t)(e0 + i) * d)[k];
+                const float2 t = dot8_bf(gq, xq, make_float2(0.f, 0.f));
                 acc[i] += t.x + t.y;
               }
           }
@@ -270,7 +286,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects
         float z = 0.f;
         if (lane < n)
-          for (int w = 0; w < kWarpsPerStage * NS; ++w) z += zpart[w * n + lane];  // fixed order
+          for (int w = 0; w < nwc; ++w) z += zpart[w * n + lane];  // fixed order
         LaneRoute lr;
         const bool writer = b == 0;
         const int nmiss = route_decide(ra, z, ds, writer, rS, rZ, rW, &lr,
@@ -557,6 +573,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
 }
 
 }  // namespace
+
+// CTAs of the fused kernel wait on each other (h publication), so the whole grid (one CTA
+// per SM) must be resident at once: check that one CTA of this plan fits on an SM.
+int fused_blocks_per_sm(const FusedPlan& p) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, expert_fused_kernel, p.threads, p.smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return nb;
+}
 
 cudaError_t preload_fused_kernels() {
   cudaFuncAttributes fa;

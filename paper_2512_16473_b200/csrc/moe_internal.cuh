@@ -111,6 +111,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);
 
 cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl, bool coop);
 cudaError_t preload_fused_kernels();
+int fused_blocks_per_sm(const FusedPlan& p);
 
 cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl);
 

@@ -198,7 +198,7 @@ struct moe_ctx {
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
   unsigned long long* d_ts = nullptr;  // per-CTA phase timestamps (MOE_DEBUG_TS=1)
-  bool coop = true;                    // cooperative launch of the fused expert kernel
+  bool coop = false;                   // cooperative launch of the fused kernel (MOE_COOP=1)
   unsigned long long* d_sts = nullptr; // per-call step timestamps, ring of kStsRing (MOE_DEBUG_TS=1)
 };
 
@@ -538,10 +538,15 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
     const char* path = getenv("MOE_EXPERT_PATH");
     const char* pdl = getenv("MOE_PDL");
     c->pdl = !(pdl && pdl[0] == '0');
+    // The fused grid is one CTA per SM and its CTAs wait on each other, so it must be fully
+    // resident: guaranteed by the occupancy check below while nothing else holds SMs for
+    // long (MOE_COOP=1 makes the launch cooperative — the driver then checks co-residency —
+    // at the cost of the early PDL start, ~2.5 us per call).
     const char* coop = getenv("MOE_COOP");
-    c->coop = !(coop && coop[0] == '0');
+    c->coop = coop && coop[0] == '1';
     c->fused_grid = c->num_sms;
-    c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, n, K, c->fused_grid, &c->plan);
+    c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, n, K, c->fused_grid, &c->plan) &&
+               fused_blocks_per_sm(c->plan) >= 1;
     if (getenv("MOE_DEBUG_KERNEL")) {  // progress words in host-mapped memory (slow: PCIe atomics)
       INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
       memset(c->h_dbg, 0, 64);
