@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libmoe.so")
+LIB_PATH = os.environ.get("MOE_LIB_PATH") or os.path.join(_PKG, "lib", "libmoe.so")  # override: A/B runs
 
 MOE_OK = 0
 STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_OUT_OF_MEMORY", 3: "MOE_ERR_CUDA",

@@ -40,7 +40,9 @@ using namespace ptx;
 
 constexpr int kMaxNS = 10;                 // ring stages (phase B pairs them: NS even)
 constexpr int kWarpsPerStage = 2;          // consumer warps sharing one stage
-constexpr int kThreadsF = 32 * (1 + kWarpsPerStage * kMaxNS);
+constexpr int kRouterWarp = 1 + kWarpsPerStage * kMaxNS;  // warp 0 producer, 1..2NS consumers
+constexpr int kRouteBar = 13;              // named barrier: partial logits -> router warp
+constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
 constexpr int kTsPerCta = 40;             // debug timestamps per CTA (MOE_DEBUG_TS)
 
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ int snseg;
   __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
   __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
-  __shared__ __align__(8) uint64_t gbar, xbar;            // gate rows landed / x landed
+  __shared__ __align__(8) uint64_t gbar, xbar, rbar;      // gate rows landed / x landed / route published
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(hbar, 1);
     mbar_init(&gbar, 1);
     mbar_init(&xbar, 1);
+    mbar_init(&rbar, 1);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
     mbar_arrive_expect_tx(&gbar, gate_bytes);
@@ -230,105 +233,109 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         if (i < n) greg[i] = reinterpret_cast<const int4*>(gsm + (size_t)i * d)[gk0 + lane];
     }
   }
-  {
-    // Programmatic dependent launch: the previous call's kernel (cache directory,
-    // counters, h) and the caller's x are complete and visible after this wait.
-    griddep_wait();
-    if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 8] = globaltimer();
-    DirState ds;
-    if (cw == 0) ds = dir_load(ra, lane);          // the routing warp's directory loads in flight
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&xbar, 2u * d);
-      bulk_g2s(xh, a.x, 2u * d, &xbar, policy_evict_last());
-    }
-    if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
-      f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
-    if (K == 2 && cw >= 0) {  // y accumulates the two experts: zero this CTA's slice
-                              // (published to the other CTAs with this CTA's h releases)
-      const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
-      for (int c = c0 + ctid; c < c1; c += nthr) a.y[c] = 0.f;
-    }
-    mbar_wait(&xbar, 0);
-    if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 9] = globaltimer();
-    unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
-    if (pm && threadIdx.x == 32) pm[0] = clock64();
-    if (cw >= 0 && cw < kWarpsPerStage * NS) {
-      if (pm && threadIdx.x == 32) pm[1] = clock64();
-      // gate GEMV: per-warp partial sums, reduced in a fixed order by the routing warp
-      {
-        for (int e0 = 0; e0 < n; e0 += 8) {
-          float acc[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-          for (int k = gk0 + lane; k < gk1; k += 32) {
-            const int4 xq = reinterpret_cast<const int4*>(xh)[k];
-            const bool inreg = e0 == 0 && k == gk0 + lane;
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (e0 + i < n) {
-                const int4 gq = inreg ? greg[i] : reinterpret_cast<const int4*>(gsm + (size_t)(e0 + i) * d)[k];
-                const float2 t = dot8_bf(gq, xq, make_float2(0.f, 0.f));
-                acc[i] += t.x + t.y;
-              }
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float v = warp_sum(acc[i]);
-            if (lane == 0 && e0 + i < n) zpart[cw * n + e0 + i] = v;
-          }
-        }
-      }
-      if (pm && threadIdx.x == 32) pm[2] = clock64();
-      named_bar_sync(1, nthr);
-      if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 10] = globaltimer();
-      if (pm && threadIdx.x == 32) pm[3] = clock64();
-      if (cw == 0) {
-        // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects
-        float z = 0.f;
-        if (lane < n)
-          for (int w = 0; w < nwc; ++w) z += zpart[w * n + lane];  // fixed order
-        LaneRoute lr;
-        const bool writer = b == 0;
-        const int nmiss = route_decide(ra, z, ds, writer, rS, rZ, rW, &lr,
-                                       pm ? pm + 4 : nullptr);
-        if (f.ts && lane == 0) f.ts[b * kTsPerCta + 11] = globaltimer();
-        if (pm && lane == 0) pm[7] = clock64();
-        if (lane < K) {
-          sslot[lane] = lr.slot;
-          sgen[lane] = lr.gen;
-          swait[lane] = lr.wait;
-          shost[lane] = lr.host;
-          sbase[lane] = a.pool + (long long)lr.slot * a.slot_bytes;
-          swgt[lane] = lr.w;
-        }
-        // device-computed experts in processing order: resident ones first, then the ones
-        // whose fill may still be in flight (rank order within each)
-        const unsigned dev_ready = __ballot_sync(0xffffffffu, lane < K && !lr.host && !lr.wait);
-        const unsigned dev_wait = __ballot_sync(0xffffffffu, lane < K && !lr.host && lr.wait);
-        const unsigned below = (1u << lane) - 1u;
-        if (lane < K && !lr.host)
-          sorder[lr.wait ? __popc(dev_ready) + __popc(dev_wait & below) : __popc(dev_ready & below)] = lane;
-        if (lane == 0) {
-          snseg = __popc(dev_ready | dev_wait);
-          // miss mailbox entry (host-mapped): payload, system fence, seq (the fetch
-          // thread's trigger)
-          if (writer && nmiss) {
-            __threadfence_system();
-            ra.mail->seq = ra.seq;
-          }
-        }
-      }
-    }
+  // Programmatic dependent launch: the previous call's kernel (cache directory, counters,
+  // h) and the caller's x are complete and visible after this wait.
+  griddep_wait();
+  if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 8] = globaltimer();
+  DirState ds;
+  if (warp == kRouterWarp) ds = dir_load(ra, lane);  // the router's directory loads in flight
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&xbar, 2u * d);
+    bulk_g2s(xh, a.x, 2u * d, &xbar, policy_evict_last());
   }
-  __syncthreads();          // route in shared memory; gate staging area free
-  griddep_launch_dependents();
-  if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
-  const int nseg = snseg;
+  if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
+    f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
+  if (K == 2 && cw >= 0 && cw < nwc) {  // y accumulates the two experts: zero this CTA's slice
+                                        // (published to the other CTAs with its h releases)
+    const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
+    for (int c = c0 + ctid; c < c1; c += nthr) a.y[c] = 0.f;
+  }
+  unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
+  if (cw >= 0 && cw < nwc) {
+    mbar_wait(&xbar, 0);
+    if (f.ts && threadIdx.x == 32) f.ts[b * kTsPerCta + 9] = globaltimer();
+    if (pm && threadIdx.x == 32) pm[1] = clock64();
+    // gate GEMV: per-warp partial sums, reduced in a fixed order by the router warp
+    for (int e0 = 0; e0 < n; e0 += 8) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+      for (int k = gk0 + lane; k < gk1; k += 32) {
+        const int4 xq = reinterpret_cast<const int4*>(xh)[k];
+        const bool inreg = e0 == 0 && k == gk0 + lane;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (e0 + i < n) {
+            const int4 gq = inreg ? greg[i] : reinterpret_cast<const int4*>(gsm + (size_t)(e0 + i) * d)[k];
+            const float2 t = dot8_bf(gq, xq, make_float2(0.f, 0.f));
+            acc[i] += t.x + t.y;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float v = warp_sum(acc[i]);
+        if (lane == 0 && e0 + i < n) zpart[cw * n + e0 + i] = v;
+      }
+    }
+    if (pm && threadIdx.x == 32) pm[2] = clock64();
+    named_bar_arrive(kRouteBar, nthr + 32);  // partial logits ready; on to phase A
+  } else if (warp == kRouterWarp) {
+    // ---------------------------------------------------------------- router warp
+    // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects.
+    // The producer starts as soon as the slots are known (all hit: before the bookkeeping).
+    named_bar_sync(kRouteBar, nthr + 32);
+    if (f.ts && lane == 0) f.ts[b * kTsPerCta + 10] = globaltimer();
+    if (pm && lane == 0) pm[3] = clock64();
+    float z = 0.f;
+    if (lane < n)
+      for (int w = 0; w < nwc; ++w) z += zpart[w * n + lane];  // fixed order
+    bool published = false;
+    auto publish = [&](const LaneRoute& lr) {
+      if (lane < K) {
+        sslot[lane] = lr.slot;
+        sgen[lane] = lr.gen;
+        swait[lane] = lr.wait;
+        shost[lane] = lr.host;
+        sbase[lane] = a.pool + (long long)lr.slot * a.slot_bytes;
+        swgt[lane] = lr.w;
+      }
+      // device-computed experts in processing order: resident ones first, then the ones
+      // whose fill may still be in flight (rank order within each)
+      const unsigned dev_ready = __ballot_sync(0xffffffffu, lane < K && !lr.host && !lr.wait);
+      const unsigned dev_wait = __ballot_sync(0xffffffffu, lane < K && !lr.host && lr.wait);
+      const unsigned below = (1u << lane) - 1u;
+      if (lane < K && !lr.host)
+        sorder[lr.wait ? __popc(dev_ready) + __popc(dev_wait & below) : __popc(dev_ready & below)] = lane;
+      if (lane == 0) snseg = __popc(dev_ready | dev_wait);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&rbar);                // release: the route is in shared memory
+        if (f.ts) f.ts[b * kTsPerCta + 1] = globaltimer();
+      }
+      published = true;
+    };
+    LaneRoute lr;
+    const bool writer = b == 0;
+    const int nmiss = route_decide(ra, z, ds, writer, rS, rZ, rW, &lr, pm ? pm + 4 : nullptr, publish);
+    if (f.ts && lane == 0) f.ts[b * kTsPerCta + 11] = globaltimer();
+    if (pm && lane == 0) pm[7] = clock64();
+    if (!published) publish(lr);
+    // miss mailbox entry (host-mapped): payload, system fence, seq (the fetch thread's
+    // trigger)
+    if (lane == 0 && writer && nmiss) {
+      __threadfence_system();
+      ra.mail->seq = ra.seq;
+    }
+    griddep_launch_dependents();
+    return;
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
+      mbar_wait(&rbar, 0);                            // route published by the router warp
+      const int nseg = snseg;
       for (int r = 0; r < K; ++r)  // host-computed experts have no h: publish them at once
         if (shost[r]) red_release_add_u64(f.bar + 16 * r, (unsigned long long)NS);
       uint32_t use = 0;                               // per-stage use-count parity bits
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   }
 
   // -------------------------------------------------------------------- consumers
-  if (cw >= kWarpsPerStage * NS) return;
+  if (cw >= nwc) return;
   const int sA = cw >> 1, half = cw & 1;   // phase A: stage and half of the row
   uint32_t ph = 0;                         // parity of the barrier this warp waits on
   {
@@ -501,6 +508,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_wait(hbar, hph);
     hph ^= 1;
   };
+  const int nseg = snseg;                  // (visible: published before the producer's first marker)
   {
     const int u = cw >> 2, q = cw & 3;     // super-stage and quarter of the W2 row
     const bool active = u < NSB;           // (NS odd: the last stage's warps sit out phase B)

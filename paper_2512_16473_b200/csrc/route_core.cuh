@@ -54,11 +54,19 @@ struct LaneRoute {
   int host = 0;   // 1: computed by the host cores (HOST_COMPUTE miss)
 };
 
-// One full warp. sS/sW: per-warp shared scratch of >= K entries, sZ of >= n entries. Returns the number of
-// misses (the writer publishes the mailbox seq itself, after its own ordering needs).
+struct NoEarlyRoute {
+  __device__ void operator()(const LaneRoute&) const {}
+};
+
+// One full warp. sS/sW: per-warp shared scratch of >= K entries, sZ of >= n entries. Returns
+// the number of misses (the writer publishes the mailbox seq itself, after its own ordering
+// needs). When every routed expert hits, `early(lr)` is called (by the whole warp, lane r <
+// K holding rank r's final decision) as soon as the slots are known, before the cache
+// bookkeeping — the caller may start streaming then.
+template <class Early = NoEarlyRoute>
 __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum, const DirState& ds,
                                             const bool writer, int* sS, float* sZ, float* sW, LaneRoute* out,
-                                            unsigned long long* dts = nullptr) {
+                                            unsigned long long* dts = nullptr, Early early = Early()) {
   const int lane = threadIdx.x & 31;
   const int n = a.n, K = a.K, M = a.M;
   // ---- top-K by (z desc, index asc): lane e counts the experts that precede it (one
@@ -105,6 +113,23 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
     for (int r = 0; r < K; ++r) {
       const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sS[r]);
       if (lane == r) { myHit = m != 0u; myWay = m ? __ffs(m) - 1 : -1; }
+    }
+    {
+      // all K hit: slot and generation of every rank are final already (a hit never changes
+      // its way's generation)
+      const uint32_t gw = __shfl_sync(0xffffffffu, gen, myWay < 0 ? 0 : myWay);
+      if (__ballot_sync(0xffffffffu, lane < K && myHit) == (K >= 32 ? 0xffffffffu : (1u << K) - 1u)) {
+        LaneRoute e;
+        if (lane < K) {
+          e.expert = myS;
+          e.w = sW[lane];
+          e.slot = a.slot_base + myWay;
+          e.gen = gw;
+          e.wait = a.miss_mode == MOE_MISS_HOST_COMPUTE ? *((volatile const uint32_t*)(a.ready + e.slot)) < gw : 0;
+          e.host = 0;
+        }
+        early(e);
+      }
     }
     const bool is_static = a.policy == MOE_POLICY_STATIC_RANDOM;
     // step 2: touch hits in rank order (LRU; FIFO keeps insertion order; STATIC never changes)
