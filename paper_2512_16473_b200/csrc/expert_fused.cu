@@ -112,7 +112,6 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
 
 constexpr int kChunkA = 2;     // phase A rows per tail claim
 constexpr int kChunkB = 1;     // phase B rows per tail claim
-constexpr int kStaticPct = 88; // share of each segment's rows assigned statically (no atomics)
 
 // Ring-slot meta word: >= 0 a weight row (phase A: (r << 24) | j, phase B: c);
 // kEnd closes a phase; kSegB switches phase B to the next expert; kSegA - r closes
@@ -121,7 +120,7 @@ constexpr int kEnd = -1;
 constexpr int kSegB = -2;
 constexpr int kSegA = -3;
 
-// Static-then-steal schedule over `total` rows for CTA b of G: the first kStaticPct% of
+// Static-then-steal schedule over `total` rows for CTA b of G: the first pct% of
 // the rows are split into equal contiguous blocks, the tail is claimed in chunks from a
 // per-segment counter, so every CTA ends each segment within about one chunk of the
 // others, whatever its share of HBM bandwidth.
@@ -129,9 +128,9 @@ struct RowSched {
   int s0, s1;    // this CTA's static block
   int tail0;     // first tail row
 };
-__device__ __forceinline__ RowSched make_sched(int total, int b, int G) {
+__device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct) {
   RowSched rs;
-  const int sb = (int)((long long)total * kStaticPct / 100 / G);
+  const int sb = (int)((long long)total * pct / 100 / G);
   rs.s0 = b * sb;
   rs.s1 = rs.s0 + sb;
   rs.tail0 = G * sb;
@@ -164,7 +163,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ int snseg;
   __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
   __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
-  __shared__ __align__(8) uint64_t gbar, xbar, rbar;      // gate rows landed / x landed / route published
+  __shared__ __align__(8) uint64_t gbar, xbar, rbar, wbar;  // gate rows / x landed; slots / weights published
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
@@ -211,6 +210,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(&gbar, 1);
     mbar_init(&xbar, 1);
     mbar_init(&rbar, 1);
+    mbar_init(&wbar, 1);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
     mbar_arrive_expect_tx(&gbar, gate_bytes);
@@ -297,7 +297,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         swait[lane] = lr.wait;
         shost[lane] = lr.host;
         sbase[lane] = a.pool + (long long)lr.slot * a.slot_bytes;
-        swgt[lane] = lr.w;
       }
       // device-computed experts in processing order: resident ones first, then the ones
       // whose fill may still be in flight (rank order within each)
@@ -320,6 +319,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (f.ts && lane == 0) f.ts[b * kTsPerCta + 11] = globaltimer();
     if (pm && lane == 0) pm[7] = clock64();
     if (!published) publish(lr);
+    if (lane < K) swgt[lane] = lr.w;       // gate weights: needed from phase B on
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&wbar);
     // miss mailbox entry (host-mapped): payload, system fence, seq (the fetch thread's
     // trigger)
     if (lane == 0 && writer && nmiss) {
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       };
       // phase A: per segment, static block then tail claims (two claims in flight hide the
       // atomic latency)
-      const RowSched sa = make_sched(ffr, b, G);
+      const RowSched sa = make_sched(ffr, b, G, f.pctA);
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* base = sbase[r];
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           mbar_arrive(full + s);
         }
       };
-      const RowSched sbk = make_sched(d, b, G);
+      const RowSched sbk = make_sched(d, b, G, f.pctB);
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* w2 = sbase[r] + w2off;
@@ -509,6 +511,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     hph ^= 1;
   };
   const int nseg = snseg;                  // (visible: published before the producer's first marker)
+  mbar_wait(&wbar, 0);                     // gate weights (long published by now)
   {
     const int u = cw >> 2, q = cw & 3;     // super-stage and quarter of the W2 row
     const bool active = u < NSB;           // (NS odd: the last stage's warps sit out phase B)
@@ -618,6 +621,8 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;
+  p->pctA = 88;
+  p->pctB = 40;
   p->smem = (size_t)NS * SB + xh + tail;
   p->threads = kThreadsF;
   return p->smem <= (size_t)kFusedMaxDynSmem;

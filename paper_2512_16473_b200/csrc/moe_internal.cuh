@@ -99,12 +99,13 @@ struct FusedArgs {
   unsigned* ctr;                  // work-claim counters [2][kMaxK] (phase A rows, phase B rows), zeroed per call
   int NS, SB;                     // ring stages / stage bytes
   int xh_bytes;
+  int pctA, pctB;                 // share of phase A / B rows assigned statically (rest: stolen)
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
   unsigned long long* sts;        // this call's step record [kStsHead + 2*grid] (MOE_DEBUG_TS=1) or nullptr
 };
 struct FusedPlan {
-  int SB, NS, xh_bytes, threads;
+  int SB, NS, xh_bytes, threads, pctA, pctB;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

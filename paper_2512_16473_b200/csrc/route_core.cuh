@@ -61,8 +61,9 @@ struct NoEarlyRoute {
 // One full warp. sS/sW: per-warp shared scratch of >= K entries, sZ of >= n entries. Returns
 // the number of misses (the writer publishes the mailbox seq itself, after its own ordering
 // needs). When every routed expert hits, `early(lr)` is called (by the whole warp, lane r <
-// K holding rank r's final decision) as soon as the slots are known, before the cache
-// bookkeeping — the caller may start streaming then.
+// K holding rank r's final slot, generation and wait flag — not yet its gate weight) as
+// soon as the slots are known, before the softmax and the cache bookkeeping: the caller
+// may start streaming then.
 template <class Early = NoEarlyRoute>
 __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum, const DirState& ds,
                                             const bool writer, int* sS, float* sZ, float* sW, LaneRoute* out,
@@ -74,14 +75,48 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
   if (lane < n) sZ[lane] = zsum;
   __syncwarp();
   int rank = 0;
-  if (lane < n)
+  if (lane < n) {
+#pragma unroll 8
     for (int j = 0; j < n; ++j) {
       const float zj = sZ[j];
       rank += (zj > zsum) || (zj == zsum && j < lane);
     }
-  if (lane < n && rank < K) { sS[rank] = lane; sW[rank] = zsum; }
+  }
+  if (lane < n && rank < K) { sS[rank] = lane; sW[rank] = zsum; }  // sW: selected logits for now
   __syncwarp();
   if (dts && lane == 0) dts[0] = clock64();
+
+  // ---- cache probe (lane = way), step 1: partition against the pre-access state
+  const int myS = lane < K ? sS[lane] : -1;  // lane r < K carries rank r's decision
+  int myHit = 0, myWay = -1, myEv = -1, mySlot = 0;
+  uint32_t myGen = 0;
+  unsigned long long clock = 0;
+  int32_t tag = ds.tag;
+  unsigned long long st = ds.stamp;
+  uint32_t gen = ds.gen;
+  if (a.covered) {
+    clock = ds.clock;
+    for (int r = 0; r < K; ++r) {
+      const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sS[r]);
+      if (lane == r) { myHit = m != 0u; myWay = m ? __ffs(m) - 1 : -1; }
+    }
+    // all K hit: slot and generation of every rank are final already (a hit never changes
+    // its way's generation); the gate weights follow below (e.w is not set)
+    const uint32_t gw = __shfl_sync(0xffffffffu, gen, myWay < 0 ? 0 : myWay);
+    if (__ballot_sync(0xffffffffu, lane < K && myHit) == (K >= 32 ? 0xffffffffu : (1u << K) - 1u)) {
+      LaneRoute e;
+      if (lane < K) {
+        e.expert = myS;
+        e.slot = a.slot_base + myWay;
+        e.gen = gw;
+        e.wait = a.miss_mode == MOE_MISS_HOST_COMPUTE ? *((volatile const uint32_t*)(a.ready + e.slot)) < gw : 0;
+        e.host = 0;
+      }
+      early(e);
+    }
+  }
+  if (dts && lane == 0) dts[1] = clock64();
+
   // ---- softmax over the K selected logits (rank order, fp32): e_r = exp(z_r - z_0),
   // summed in rank order
   const float er = lane < K ? expf(sW[lane] - sW[0]) : 0.f;
@@ -97,40 +132,8 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
   __syncwarp();
   if (lane < K) sW[lane] = wr;
   __syncwarp();
-  if (dts && lane == 0) dts[1] = clock64();
 
-  // ---- cache probe + LRU update (lane = way)
-  const int myS = lane < K ? sS[lane] : -1;  // lane r < K carries rank r's decision
-  int myHit = 0, myWay = -1, myEv = -1, mySlot = 0;
-  uint32_t myGen = 0;
-  unsigned long long clock = 0;
   if (a.covered) {
-    int32_t tag = ds.tag;
-    unsigned long long st = ds.stamp;
-    uint32_t gen = ds.gen;
-    clock = ds.clock;
-    // step 1: partition against the pre-access state
-    for (int r = 0; r < K; ++r) {
-      const unsigned m = __ballot_sync(0xffffffffu, lane < M && tag == sS[r]);
-      if (lane == r) { myHit = m != 0u; myWay = m ? __ffs(m) - 1 : -1; }
-    }
-    {
-      // all K hit: slot and generation of every rank are final already (a hit never changes
-      // its way's generation)
-      const uint32_t gw = __shfl_sync(0xffffffffu, gen, myWay < 0 ? 0 : myWay);
-      if (__ballot_sync(0xffffffffu, lane < K && myHit) == (K >= 32 ? 0xffffffffu : (1u << K) - 1u)) {
-        LaneRoute e;
-        if (lane < K) {
-          e.expert = myS;
-          e.w = sW[lane];
-          e.slot = a.slot_base + myWay;
-          e.gen = gw;
-          e.wait = a.miss_mode == MOE_MISS_HOST_COMPUTE ? *((volatile const uint32_t*)(a.ready + e.slot)) < gw : 0;
-          e.host = 0;
-        }
-        early(e);
-      }
-    }
     const bool is_static = a.policy == MOE_POLICY_STATIC_RANDOM;
     // step 2: touch hits in rank order (LRU; FIFO keeps insertion order; STATIC never changes)
     for (int r = 0; r < K; ++r) {

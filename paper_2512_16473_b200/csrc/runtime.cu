@@ -547,6 +547,12 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
     c->fused_grid = c->num_sms;
     c->fused = !(path && strcmp(path, "split") == 0) && plan_fused(d, c->ffr, n, K, c->fused_grid, &c->plan) &&
                fused_blocks_per_sm(c->plan) >= 1;
+    if (c->fused) {  // schedule knobs (experiments): static share of phase A / B rows, percent
+      const char* pa = getenv("MOE_STATIC_A");
+      const char* pb = getenv("MOE_STATIC_B");
+      if (pa && atoi(pa) >= 0 && atoi(pa) <= 100) c->plan.pctA = atoi(pa);
+      if (pb && atoi(pb) >= 0 && atoi(pb) <= 100) c->plan.pctB = atoi(pb);
+    }
     if (getenv("MOE_DEBUG_KERNEL")) {  // progress words in host-mapped memory (slow: PCIe atomics)
       INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
       memset(c->h_dbg, 0, 64);
@@ -831,6 +837,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.NS = c->plan.NS;
     fa.SB = c->plan.SB;
     fa.xh_bytes = c->plan.xh_bytes;
+    fa.pctA = c->plan.pctA;
+    fa.pctB = c->plan.pctB;
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
     fa.sts = ra.sts;
