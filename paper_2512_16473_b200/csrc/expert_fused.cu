@@ -78,6 +78,16 @@ __device__ __forceinline__ float2 dot8_bf(const int4 w, const int4 x, float2 acc
   return acc;
 }
 
+// D(16x8, fp32) += A(16x16, bf16, row) * B(16x8, bf16, col): warp-level tensor-core MMA
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 // bf16 pair (one 32-bit word) -> (lo, hi) fp32, exact
 __device__ __forceinline__ float2 bf2(uint32_t v) { return make_float2(bf_lo(v), bf_hi(v)); }
 
@@ -187,9 +197,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   // work-claim counters of this call ([A r][B r]); the other parity is zeroed for the next
   unsigned* ctr = f.ctr + (f.calls & 1) * (2 * kMaxFusedK);
   // the ring is free until the route is known: it stages the gate rows and x first
-  const uint32_t gate_bytes = (uint32_t)n * (uint32_t)d * 2u;
-  const uint16_t* gsm = reinterpret_cast<const uint16_t*>(ring);
-  float* zpart = reinterpret_cast<float*>(ring + gate_bytes);  // [consumer warp][n] partial logits
+  // gate rows at a padded stride (+16 B: the 8 rows of an MMA fragment hit distinct banks)
+  const int gstride = 2 * d + 16;
+  float* zpart = reinterpret_cast<float*>(ring + (size_t)n * gstride);  // [consumer warp][n] partial logits
   // x (bf16) lives in xh through phase A; phase B reuses xh for h_r (fp32)
   const int cw = warp - 1;                      // consumer warp 0 .. 2*NS-1 (warp 0: producer)
   const int nthr = kWarpsPerStage * NS * 32;
@@ -213,26 +223,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(&wbar, 1);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
-    mbar_arrive_expect_tx(&gbar, gate_bytes);
-    bulk_g2s(ring, f.r.Wg, gate_bytes, &gbar, policy_evict_last());
+    const uint64_t pl = policy_evict_last();
+    mbar_arrive_expect_tx(&gbar, (uint32_t)n * 2u * d);
+    for (int e = 0; e < n; ++e) bulk_g2s(ring + (size_t)e * gstride, f.r.Wg + (size_t)e * d, 2u * d, &gbar, pl);
   }
   if (threadIdx.x == 32) ra = f.r;  // kernel parameters -> shared memory before the PDL wait
   __syncthreads();          // mbarrier inits and routing arguments visible
-  // Gate GEMV z = Wg x: consumer warp w covers 16-B chunks [k0, k1) of every row, a
-  // lane one x chunk against all n gate rows. The first chunk of the first 8 rows is held in
-  // registers, loaded before the PDL wait (the gate is constant across calls).
   const int nwc = kWarpsPerStage * NS;
-  const int nch = d >> 3, cpw = (nch + nwc - 1) / nwc;
-  const int gk0 = cw * cpw, gk1 = min(nch, gk0 + cpw);
-  int4 greg[8];
-  if (cw >= 0 && cw < nwc) {
-    mbar_wait(&gbar, 0);
-    if (gk0 + lane < gk1) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i < n) greg[i] = reinterpret_cast<const int4*>(gsm + (size_t)i * d)[gk0 + lane];
-    }
-  }
   // Programmatic dependent launch: the previous call's kernel (cache directory, counters,
   // h) and the caller's x are complete and visible after this wait.
   griddep_wait();
@@ -255,26 +252,33 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_wait(&xbar, 0);
     if (f.ts && threadIdx.x == 32) f.ts[b * kTsPerCta + 9] = globaltimer();
     if (pm && threadIdx.x == 32) pm[1] = clock64();
-    // gate GEMV: per-warp partial sums, reduced in a fixed order by the router warp
-    for (int e0 = 0; e0 < n; e0 += 8) {
-      float acc[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-      for (int k = gk0 + lane; k < gk1; k += 32) {
-        const int4 xq = reinterpret_cast<const int4*>(xh)[k];
-        const bool inreg = e0 == 0 && k == gk0 + lane;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (e0 + i < n) {
-            const int4 gq = inreg ? greg[i] : reinterpret_cast<const int4*>(gsm + (size_t)(e0 + i) * d)[k];
-            const float2 t = dot8_bf(gq, xq, make_float2(0.f, 0.f));
-            acc[i] += t.x + t.y;
-          }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float v = warp_sum(acc[i]);
-        if (lane == 0 && e0 + i < n) zpart[cw * n + e0 + i] = v;
+    // Gate GEMV z = Wg x on the tensor cores: mma.sync m16n8k16 (bf16 in, fp32
+    // accumulate), A = 16 gate rows, B = x in every column; consumer warp w takes 16-wide
+    // k-steps [ks0, ks1). Per-warp partials, reduced in a fixed order by the router warp.
+    mbar_wait(&gbar, 0);
+    {
+      const int g = lane >> 2, t = lane & 3;
+      const int ksteps = d >> 4, kps = (ksteps + nwc - 1) / nwc;
+      const int ks0 = cw * kps, ks1 = min(ksteps, ks0 + kps);
+      for (int e0 = 0; e0 < n; e0 += 16) {
+        const bool r0 = e0 + g < n, r1 = e0 + 8 + g < n;
+        const uint8_t* A0 = ring + (size_t)(e0 + g) * gstride;
+        const uint8_t* A1 = ring + (size_t)(e0 + 8 + g) * gstride;
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int ks = ks0; ks < ks1; ++ks) {
+          const int kb = (ks * 16 + 2 * t) * 2;   // byte offset of this thread's k pair
+          const uint32_t a0 = r0 ? *reinterpret_cast<const uint32_t*>(A0 + kb) : 0u;
+          const uint32_t a2 = r0 ? *reinterpret_cast<const uint32_t*>(A0 + kb + 16) : 0u;
+          const uint32_t a1 = r1 ? *reinterpret_cast<const uint32_t*>(A1 + kb) : 0u;
+          const uint32_t a3 = r1 ? *reinterpret_cast<const uint32_t*>(A1 + kb + 16) : 0u;
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xh + kb);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xh + kb + 16);
+          mma_bf16_16816(c, a0, a1, a2, a3, b0, b1);
+        }
+        if (t == 0) {
+          if (r0) zpart[cw * n + e0 + g] = c[0];
+          if (r1) zpart[cw * n + e0 + 8 + g] = c[2];
+        }
       }
     }
     if (pm && threadIdx.x == 32) pm[2] = clock64();
@@ -615,9 +619,9 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   NS &= ~1;                                      // stages pair into super-stages in phase B
   if (NS < 4) return false;
   // the gate rows and x are staged in the (still empty) ring before the route is known
-  const long long gate = 2ll * n * d;                                   // staged in the ring
+  const long long gate = (2ll * d + 16) * n;                            // staged in the ring
   const long long zp = 4ll * kWarpsPerStage * kMaxNS * MOE_MAX_EXPERTS;  // partial logits
-  if (n > MOE_MAX_EXPERTS || gate + zp > (long long)NS * SB || gate + 2ll * d >= (1ll << 20)) return false;
+  if (n > MOE_MAX_EXPERTS || d % 16 || gate + zp > (long long)NS * SB || 2ll * n * d >= (1ll << 20)) return false;
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;
