@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(hbar, 1);
     mbar_init(&gbar, 1);
     mbar_init(&xbar, 1);
-    mbar_init(&rbar, 1);
-    mbar_init(&wbar, 1);
+    mbar_init(&rbar, 32);  // every router lane arrives after its own shared-memory writes
+    mbar_init(&wbar, 32);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
     const uint64_t pl = policy_evict_last();
@@ -310,11 +310,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       if (lane < K && !lr.host)
         sorder[lr.wait ? __popc(dev_ready) + __popc(dev_wait & below) : __popc(dev_ready & below)] = lane;
       if (lane == 0) snseg = __popc(dev_ready | dev_wait);
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&rbar);                // release: the route is in shared memory
-        if (f.ts) f.ts[b * kTsPerCta + 1] = globaltimer();
-      }
+      mbar_arrive(&rbar);                  // release (each lane its own writes): route published
+      if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
       published = true;
     };
     LaneRoute lr;
@@ -324,8 +321,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (pm && lane == 0) pm[7] = clock64();
     if (!published) publish(lr);
     if (lane < K) swgt[lane] = lr.w;       // gate weights: needed from phase B on
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&wbar);
+    mbar_arrive(&wbar);
     // miss mailbox entry (host-mapped): payload, system fence, seq (the fetch thread's
     // trigger)
     if (lane == 0 && writer && nmiss) {
