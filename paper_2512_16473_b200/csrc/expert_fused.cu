@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_wait(&gbar, 0);
     {
       const int g = lane >> 2, t = lane & 3;
-      const int ksteps = d >> 4, kps = (ksteps + nwc - 1) / nwc;
+      const int ksteps = (d + 15) >> 4, kps = (ksteps + nwc - 1) / nwc;  // d % 16 == 8: half a last step
       const int ks0 = cw * kps, ks1 = min(ksteps, ks0 + kps);
       for (int e0 = 0; e0 < n; e0 += 16) {
         const bool r0 = e0 + g < n, r1 = e0 + 8 + g < n;
@@ -267,12 +267,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         float c[4] = {0.f, 0.f, 0.f, 0.f};
         for (int ks = ks0; ks < ks1; ++ks) {
           const int kb = (ks * 16 + 2 * t) * 2;   // byte offset of this thread's k pair
+          const bool hi = ks * 16 + 8 < d;         // upper 8 columns of the step inside the row
           const uint32_t a0 = r0 ? *reinterpret_cast<const uint32_t*>(A0 + kb) : 0u;
-          const uint32_t a2 = r0 ? *reinterpret_cast<const uint32_t*>(A0 + kb + 16) : 0u;
+          const uint32_t a2 = r0 && hi ? *reinterpret_cast<const uint32_t*>(A0 + kb + 16) : 0u;
           const uint32_t a1 = r1 ? *reinterpret_cast<const uint32_t*>(A1 + kb) : 0u;
-          const uint32_t a3 = r1 ? *reinterpret_cast<const uint32_t*>(A1 + kb + 16) : 0u;
+          const uint32_t a3 = r1 && hi ? *reinterpret_cast<const uint32_t*>(A1 + kb + 16) : 0u;
           const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xh + kb);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xh + kb + 16);
+          const uint32_t b1 = hi ? *reinterpret_cast<const uint32_t*>(xh + kb + 16) : 0u;
           mma_bf16_16816(c, a0, a1, a2, a3, b0, b1);
         }
         if (t == 0) {
@@ -617,7 +618,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   // the gate rows and x are staged in the (still empty) ring before the route is known
   const long long gate = (2ll * d + 16) * n;                            // staged in the ring
   const long long zp = 4ll * kWarpsPerStage * kMaxNS * MOE_MAX_EXPERTS;  // partial logits
-  if (n > MOE_MAX_EXPERTS || d % 16 || gate + zp > (long long)NS * SB || 2ll * n * d >= (1ll << 20)) return false;
+  if (n > MOE_MAX_EXPERTS || d % 8 || gate + zp > (long long)NS * SB || 2ll * n * d >= (1ll << 20)) return false;
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;

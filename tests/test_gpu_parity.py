@@ -413,3 +413,37 @@ def test_prefill_mixtral_layer_256_tokens():
         np.testing.assert_array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
     worst = max(float(np.abs(y[t, 0] - ref.y[t, 0]).max() / np.abs(ref.y[t, 0]).max()) for t in range(T))
     assert worst <= TOL, worst
+
+
+@pytest.mark.parametrize("L,d,ff,n,K,M,T", [(2, 72, 40, 32, 1, 2, 30), (2, 136, 64, 12, 1, 3, 24),
+                                            (3, 4104, 64, 8, 2, 4, 12)])
+def test_fused_path_odd_shapes(L, d, ff, n, K, M, T):
+    """The one-kernel step on shapes off its fast grid: K = 1 (store combine), d % 16 == 8
+    (half a last tensor-core k-step), n = 32 gate rows, d > 4096 (two k-steps per lane)."""
+    hm = harness.host_model(L, d, ff, n, K)
+    x, ranked = harness.hidden_states(hm, T, "paper")
+    ref = _oracle_run(hm, x, N=L, M=M)
+    with harness.open_moe(hm) as m:
+        assert m.runtime_info()["expert_path"] == "fused"
+        m.configure(ways=M, indexes=L)
+        y = harness.run_decode(m, x)
+        _compare(hm, m, x, ref, y)
+
+
+@pytest.mark.parametrize("env", [{"MOE_EXPERT_PATH": "split"}, {"MOE_COOP": "1"}, {"MOE_PDL": "0"},
+                                 {"MOE_STATIC_A": "0", "MOE_STATIC_B": "0"},
+                                 {"MOE_STATIC_A": "100", "MOE_STATIC_B": "100"}])
+def test_launch_and_schedule_variants(tiny, monkeypatch, env):
+    """Every launch / schedule variant the runtime can take gives the same bit-exact trace and
+    outputs: the split fallback, the cooperative launch, no PDL, all-stolen and all-static
+    row schedules (the work-claim counters at their extremes)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x, ranked = harness.hidden_states(tiny, 24, "paper")
+    ref = _oracle_run(tiny, x, N=3, M=2)
+    with harness.open_moe(tiny) as m:
+        info = m.runtime_info()
+        assert info["expert_path"] == ("split" if "MOE_EXPERT_PATH" in env else "fused")
+        m.configure(ways=2, indexes=3)
+        y = harness.run_decode(m, x)
+        _compare(tiny, m, x, ref, y)
