@@ -5,8 +5,8 @@ expert SwiGLU GEMVs + combine) per token, through the C-ABI.
 N=1 workload = BASELINE.json configs[1]: a single Mixtral-8x7B-shaped MoE layer
 (d=4096, ff=14336, 8 experts, top-2), decode batch 1, 8-way cache warm (all experts
 resident), routing from the paper-pattern generator. N>1 (torchrun): the same layer with
-each expert's ff dimension split across the N ranks + a per-layer NCCL all-reduce
-(north_star (4)); total work fixed ("strong").
+each expert's ff dimension split across the N ranks, y summed inside the decode kernel
+over peer memory (f3; NCCL all-reduce fallback) (north_star (4)); total work fixed ("strong").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -192,6 +192,16 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     yd = torch.empty((TRACE_TOKENS, CFG["d"]), dtype=torch.float32, device=dev)
     m = harness.open_moe(hm, device=local_rank, nccl_id=nccl_id)
     m.configure(ways=CFG["n"], indexes=1, warm_start=True)
+    tp_reduce = None
+    if world > 1:
+        # f3: y summed inside the decode kernel over peer memory (CUDA IPC over NVLink);
+        # every rank falls back to the NCCL all-reduce together if any rank cannot map its peers
+        if os.environ.get("MOE_TP_REDUCE", "fused") == "nccl":
+            tp_reduce = "nccl all-reduce after the kernel (MOE_TP_REDUCE=nccl)"
+        else:
+            r = tp.connect_peers(m)
+            tp_reduce = ("fused peer-memory reduction in the decode kernel's epilogue" if r == "fused-peer"
+                         else f"nccl all-reduce after the kernel (fused peer reduction unavailable: {r})")
     stream = torch.cuda.Stream(dev)
     sp = stream.cuda_stream
 
@@ -275,7 +285,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     rt_ms = rt["ms"] / max(rt["launches"], 1)
     kname = "expert_fused (router + cache probe + gate/up + down + combine)" if fused else "expert_gateup"
     kbytes = step_bytes if fused else bytes_gateup
-    if fused and world == 1:
+    if fused and (world == 1 or rinfo.get("tp_reduce") == "fused-peer"):
         # the timed region holds exactly K back-to-back launches of this one kernel and
         # nothing else: its average launch duration is the region's event time / K
         launch_ms = ms_step
@@ -294,7 +304,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         "data": "synthetic (seeded counter-based bf16 weights of Mixtral-8x7B expert shape, paper-pattern routing, "
                 "margin-guaranteed hidden states)",
         "config": {"workload": WORKLOAD, "cache": f"N=1 index, M={CFG['n']} ways, warm (all hits)",
-                   "parallelism": f"tp{world} (expert ff-split + NCCL all-reduce)" if world > 1 else "single GPU",
+                   "parallelism": f"tp{world} (expert ff-split; {tp_reduce})" if world > 1 else "single GPU",
                    "trace_tokens": TRACE_TOKENS, "runtime": rinfo, "routing": "paper preset (p_token_reuse=0.15)",
                    "l2": f"inputs larger than L2: {step_bytes / 1e6:.1f} MB of expert weights per step vs 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,

@@ -61,7 +61,9 @@ typedef struct moe_ctx moe_ctx; /* opaque; created by moe_init, freed by moe_des
  *  ranks (north_star (4)); ff % (8 * P) == 0; rank tp_rank holds rows
  *  [tp_rank*ff/P, (tp_rank+1)*ff/P) of W1/W3 and the matching columns of W2.
  *  nccl_unique_id: 128 bytes from moe_nccl_unique_id() on rank 0, broadcast by the
- *  caller (e.g. torch.distributed); must be NULL iff tp_size == 1. */
+ *  caller (e.g. torch.distributed); must be NULL if tp_size == 1. NULL with tp_size > 1
+ *  means no NCCL communicator: the y reduction must then be the fused peer-memory one
+ *  (moe_tp_connect_ipc / moe_tp_connect_local) before the first forward. */
 typedef struct {
   int32_t num_layers, d_model, d_ff, num_experts, top_k;
   int32_t device;
@@ -232,9 +234,12 @@ MOE_API moe_status moe_profile_read(moe_ctx* ctx, moe_profile_t* out);
 /* Which kernels this context launches (diagnostics): expert_path 1 = fused persistent
  * expert kernel (bulk-copy ring, grid barrier), 0 = split gate/up + down kernels (used
  * when the fused plan does not fit shared memory); pdl = programmatic dependent launch
- * in use; ring_stages / stage_bytes / grid of the fused kernel. */
+ * in use; ring_stages / stage_bytes / grid of the fused kernel; tp_reduce = how a
+ * tensor-parallel y is summed: 0 none (tp_size 1, or P > 1 with neither NCCL nor a
+ * connected exchange yet), 1 ncclAllReduce after the kernel,
+ * 2 fused peer-memory reduction in the kernel's epilogue (moe_tp_connect_*). */
 typedef struct {
-  int32_t expert_path, pdl, ring_stages, stage_bytes, grid, reserved[3];
+  int32_t expert_path, pdl, ring_stages, stage_bytes, grid, tp_reduce, reserved[2];
 } moe_runtime_info;
 MOE_API moe_status moe_get_runtime_info(moe_ctx* ctx, moe_runtime_info* out);
 
@@ -251,6 +256,51 @@ MOE_API moe_status moe_host_free(void* p);
 
 /* 128-byte NCCL unique id for a TP group (dlopens libnccl.so.2). */
 MOE_API moe_status moe_nccl_unique_id(uint8_t* out128);
+
+/* Fused tensor-parallel reduction over peer memory (north_star (4)).
+ * The per-layer sum y = sum_p y^(p) of the ff-split (every rank holds the ff/P slice of
+ * every expert) moves INTO the decode kernel's epilogue instead of a separate
+ * ncclAllReduce launch: each rank's CTAs finish their partial y^(p) in HBM, pass a
+ * grid-wide counter, then store their column slice of y^(p) into slot [p] of EVERY
+ * rank's exchange buffer (plain stores over NVLink P2P / NVSwitch; a local store for p
+ * itself), release a per-rank arrival counter on every rank (system scope), wait until
+ * all P ranks' slices have arrived in their own buffer, and write
+ *   y[c] = (((0 + y^(0)[c]) + y^(1)[c]) + ...) + y^(P-1)[c]      (fixed rank order)
+ * so all ranks get bit-identical y (their next layer's routing stays identical).
+ * The exchange buffer is double-buffered by call parity, so a rank running one call ahead
+ * never overwrites slots a peer is still reading; counters are monotonic (no resets).
+ * Scope: the fused decode path (K <= 2; moe_get_runtime_info expert_path == 1), both miss
+ * modes. The split fallback and moe_layer_prefill keep the NCCL all-reduce (they need a
+ * communicator: pass nccl_unique_id).
+ *
+ * Setup, after moe_init on every rank and before the first forward:
+ *   multi-process (one GPU per process): moe_tp_exchange_buffer on every rank -> all-gather
+ *     the 64-byte CUDA IPC handles (e.g. torch.distributed) -> moe_tp_connect_ipc on every
+ *     rank -> a barrier across ranks (each rank zeroes its own counters in connect).
+ *   one process (several contexts; e.g. P ranks emulated on ONE GPU, or P GPUs driven by one
+ *     process): moe_tp_connect_local with all P contexts. Contexts on the same device then
+ *     split the SMs (grid = #SMs / P each, so the P grids are co-resident) and launch without
+ *     PDL; their calls for one layer must be enqueued for all ranks before any rank's next
+ *     call is waited on.
+ * With a connected exchange, tp_size > 1 contexts may be created with nccl_unique_id NULL
+ * (then only the fused decode path is available). Deadlock note: every rank must make the
+ * same sequence of forward calls; a rank whose peer never arrives traps after 60 s. */
+typedef struct {
+  void* dev_ptr;          /* this rank's exchange buffer (device memory, library-owned) */
+  int64_t bytes;          /* 256 + 2 * P * d * 4 */
+  uint8_t ipc_handle[64]; /* cudaIpcMemHandle_t of dev_ptr */
+} moe_tp_exchange;
+MOE_API moe_status moe_tp_exchange_buffer(moe_ctx* ctx, moe_tp_exchange* out);
+/* handles: [P][64] IPC handles of ranks 0..P-1 (this rank's own entry is ignored). Opens the
+ * peers' buffers (cudaIpcOpenMemHandle, closed in moe_destroy) and zeroes this rank's
+ * counters. MOE_ERR_STATE if tp_size == 1; MOE_ERR_UNSUPPORTED if the fused path is off. */
+MOE_API moe_status moe_tp_connect_ipc(moe_ctx* ctx, const uint8_t* handles);
+/* ctxs: the P contexts of one TP group (any order; tp_rank must be a permutation of 0..P-1,
+ * all with the same shape and tp_size == P). Enables peer access between distinct devices. */
+MOE_API moe_status moe_tp_connect_local(moe_ctx* const* ctxs, int32_t P);
+/* Back to the NCCL all-reduce (or to no reduction without a communicator): closes the
+ * peers' IPC mappings. Use it on every rank when one rank's connect failed. Synchronizes. */
+MOE_API moe_status moe_tp_disconnect(moe_ctx* ctx);
 
 MOE_API const char* moe_last_error(void);
 MOE_API int32_t moe_abi_version(void);

@@ -16,7 +16,7 @@ from ._abi import (MISS_FETCH, MISS_HOST_COMPUTE, POLICY_FIFO, POLICY_LRU, POLIC
                    RECORD_DTYPE, STAT_FIELDS)
 
 __all__ = ["Moe", "MoeError", "PinnedBuffer", "MISS_FETCH", "MISS_HOST_COMPUTE", "host_expert_ffn", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
-           "STAT_FIELDS", "slot_bytes", "blob_views", "lib", "nccl_unique_id", "PROF_KINDS"]
+           "STAT_FIELDS", "slot_bytes", "blob_views", "lib", "nccl_unique_id", "PROF_KINDS", "tp_connect_local"]
 
 _lib = None
 
@@ -87,6 +87,13 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     _check("moe_nccl_unique_id", lib().moe_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def tp_connect_local(moes) -> None:
+    """Connect the P contexts of one TP group living in this process (moe_tp_connect_local);
+    contexts on one GPU then split its SMs (ranks emulated on one device)."""
+    arr = (ctypes.c_void_p * len(moes))(*[m._h.value for m in moes])
+    _check("moe_tp_connect_local", lib().moe_tp_connect_local(arr, len(moes)))
 
 
 def _addr(a) -> int:
@@ -192,7 +199,25 @@ class Moe:
         r = _abi.RuntimeInfo()
         _check("moe_get_runtime_info", lib().moe_get_runtime_info(self._h, ctypes.byref(r)))
         return {"expert_path": "fused" if r.expert_path else "split", "pdl": bool(r.pdl),
-                "ring_stages": r.ring_stages, "stage_bytes": r.stage_bytes, "grid": r.grid}
+                "ring_stages": r.ring_stages, "stage_bytes": r.stage_bytes, "grid": r.grid,
+                "tp_reduce": {0: "none", 1: "nccl", 2: "fused-peer"}.get(r.tp_reduce, r.tp_reduce)}
+
+    # ------------------------------------------------------------------ fused TP reduction (f3)
+    def tp_exchange_buffer(self) -> dict:
+        """This rank's exchange buffer: {"dev_ptr", "bytes", "ipc_handle" (64 bytes)}."""
+        e = _abi.TpExchange()
+        _check("moe_tp_exchange_buffer", lib().moe_tp_exchange_buffer(self._h, ctypes.byref(e)))
+        return {"dev_ptr": e.dev_ptr, "bytes": e.bytes, "ipc_handle": bytes(e.ipc_handle)}
+
+    def tp_connect_ipc(self, handles) -> None:
+        """handles: the P ranks' 64-byte IPC handles in rank order (all-gathered by the caller)."""
+        if len(handles) != self.tp_size or any(len(h) != 64 for h in handles):
+            raise ValueError("need tp_size 64-byte IPC handles")
+        buf = (ctypes.c_uint8 * (64 * self.tp_size))(*b"".join(handles))
+        _check("moe_tp_connect_ipc", lib().moe_tp_connect_ipc(self._h, buf))
+
+    def tp_disconnect(self) -> None:
+        _check("moe_tp_disconnect", lib().moe_tp_disconnect(self._h))
 
     def profile(self, enable: bool = True) -> None:
         _check("moe_profile_enable", lib().moe_profile_enable(self._h, int(enable)))

@@ -23,7 +23,8 @@ EXPORTS = ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward",
            "moe_layer_forward_host", "cache_stats", "cache_trace", "moe_profile_enable",
            "moe_profile_read", "moe_nccl_unique_id", "moe_last_error", "moe_abi_version",
            "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn",
-           "moe_layer_prefill")
+           "moe_layer_prefill", "moe_tp_exchange_buffer", "moe_tp_connect_ipc", "moe_tp_connect_local",
+           "moe_tp_disconnect")
 
 
 class ModelDesc(ctypes.Structure):
@@ -62,7 +63,12 @@ class LayerStats(ctypes.Structure):
 
 class RuntimeInfo(ctypes.Structure):
     _fields_ = [("expert_path", ctypes.c_int32), ("pdl", ctypes.c_int32), ("ring_stages", ctypes.c_int32),
-                ("stage_bytes", ctypes.c_int32), ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("stage_bytes", ctypes.c_int32), ("grid", ctypes.c_int32), ("tp_reduce", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
+
+
+class TpExchange(ctypes.Structure):
+    _fields_ = [("dev_ptr", ctypes.c_void_p), ("bytes", ctypes.c_int64), ("ipc_handle", ctypes.c_uint8 * 64)]
 
 
 class Profile(ctypes.Structure):
@@ -98,11 +104,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.moe_host_free.argtypes = [p]
     lib.moe_host_expert_ffn.argtypes = [p, p, i32, i32, p, i32]
     lib.moe_layer_prefill.argtypes = [p, i32, p, p, i32, p]
+    lib.moe_tp_exchange_buffer.argtypes = [p, ctypes.POINTER(TpExchange)]
+    lib.moe_tp_connect_ipc.argtypes = [p, p]
+    lib.moe_tp_connect_local.argtypes = [p, i32]
+    lib.moe_tp_disconnect.argtypes = [p]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_abi_version.restype = i32
-    for name in ("moe_init", "moe_destroy", "cache_configure", "moe_layer_forward", "moe_layer_forward_host",
-                 "cache_stats", "cache_trace", "moe_profile_enable", "moe_profile_read", "moe_nccl_unique_id",
-                 "moe_get_runtime_info", "moe_host_alloc", "moe_host_free", "moe_host_expert_ffn",
-           "moe_layer_prefill"):
-        getattr(lib, name).restype = i32
+    for name in EXPORTS:
+        if name not in ("moe_last_error", "moe_abi_version"):
+            getattr(lib, name).restype = i32
     return lib

@@ -120,6 +120,68 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// 60 s without progress on a cross-CTA / cross-rank wait: fail loudly (trap), never hang
+__device__ __forceinline__ void spin_until_gpu(const unsigned long long* p, unsigned long long target) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_u64(p) < target) {
+    __nanosleep(32);
+    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+  }
+}
+__device__ __forceinline__ void spin_until_sys(const unsigned long long* p, unsigned long long target) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys_u64(p) < target) {
+    __nanosleep(32);
+    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+  }
+}
+
+// f3: fused tensor-parallel reduction of y over the ranks' exchange buffers (moe.h,
+// moe_tp_connect_*). Called by the consumer threads (ctid 0 .. nthr-1) of every CTA after
+// their last reduction into this rank's partial y^(p) (f.e.y).
+//  1. local grid barrier: every CTA's y^(p) reductions are complete (release/acquire on a
+//     monotonic counter; the CTAs are co-resident, see fused_blocks_per_sm)
+//  2. CTA b pushes its column slice [c0, c1) of y^(p) into slots[par][p] of every rank
+//     (P2P stores over NVLink; a local store for its own rank), then one thread releases
+//     (system scope, after a system fence) the slice's column count on every rank's
+//     arrival counter
+//  3. wait until this rank's arrival counter shows all P*d columns of this call, then
+//     y[c] = sum over source ranks in fixed order (bit-identical on every rank).
+__device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, int G, int ctid, int nthr) {
+  const int P = f.tpP, d = f.e.d;
+  uint8_t* own = f.peer[f.tp_rank];
+  unsigned long long* arrive = reinterpret_cast<unsigned long long*>(own);
+  unsigned long long* lbar = reinterpret_cast<unsigned long long*>(own + 16);
+  const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
+  const int par = (int)(f.tp_calls & 1);
+  named_bar_sync(1, nthr);                     // this CTA's reductions into y^(p) issued
+  if (ctid == 0) {
+    __threadfence();
+    red_release_add_u64(lbar, 1ull);
+    spin_until_gpu(lbar, (f.tp_calls + 1) * (unsigned long long)G);
+  }
+  named_bar_sync(1, nthr);
+  const long long slot_off = kTpSlotOff + ((long long)(par * P + f.tp_rank) * d) * 4;
+  for (int c = c0 + ctid; c < c1; c += nthr) {
+    const float v = __ldcg(f.e.y + c);
+    for (int p = 0; p < P; ++p) __stcg(reinterpret_cast<float*>(f.peer[p] + slot_off) + c, v);
+  }
+  named_bar_sync(1, nthr);                     // slice stored to every rank
+  if (ctid == 0) {
+    __threadfence_system();
+    for (int p = 0; p < P; ++p)
+      red_release_sys_add_u64(reinterpret_cast<unsigned long long*>(f.peer[p]), (unsigned long long)(c1 - c0));
+    spin_until_sys(arrive, (f.tp_calls + 1) * (unsigned long long)P * (unsigned long long)d);
+  }
+  named_bar_sync(1, nthr);
+  const float* slots = reinterpret_cast<const float*>(own + kTpSlotOff) + (long long)par * P * d;
+  for (int c = c0 + ctid; c < c1; c += nthr) {
+    float s = 0.f;
+    for (int p = 0; p < P; ++p) s += __ldcg(slots + (long long)p * d + c);
+    f.yout[c] = s;
+  }
+}
+
 constexpr int kChunkA = 2;     // phase A rows per tail claim
 constexpr int kChunkB = 1;     // phase B rows per tail claim
 
@@ -580,6 +642,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
     }
   }
+  if (f.tpP > 1) tp_reduce_epilogue(f, b, G, ctid, nthr);
   if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 5] = globaltimer();
   if (f.sts && cw == 0 && lane == 0) f.sts[kStsHead + G + b] = globaltimer();
 }

@@ -167,6 +167,13 @@ struct moe_ctx {
   bool any_call = false;
   // TP
   ncclComm_t comm = nullptr;
+  // fused peer-memory TP reduction (f3, moe_tp_connect_*)
+  uint8_t* d_xchg = nullptr;          // this rank's exchange buffer (tp_xchg_bytes)
+  float* d_ypart = nullptr;           // this rank's partial y^(p) [d]
+  uint8_t* tp_peer[8] = {};           // exchange buffers of ranks 0..P-1 (own included)
+  std::vector<void*> ipc_opened;      // peers' buffers opened with cudaIpcOpenMemHandle
+  bool tp_fused = false;
+  unsigned long long tp_calls = 0;
   // fused persistent expert kernel
   bool fused = false, pdl = true;
   FusedPlan plan{};
@@ -457,8 +464,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
     return fail(MOE_ERR_INVALID_ARG, "bad shape (need L>=1, d%8==0, 1<=K<=n<=32)");
   if (!(P == 1 || P == 2 || P == 4 || P == 8) || rank < 0 || rank >= P || ff % (8 * P))
     return fail(MOE_ERR_INVALID_ARG, "bad tensor-parallel split (P in {1,2,4,8}, ff % (8P) == 0)");
-  if ((P == 1) != (desc->nccl_unique_id == nullptr))
-    return fail(MOE_ERR_INVALID_ARG, "nccl_unique_id must be NULL iff tp_size == 1");
+  if (P == 1 && desc->nccl_unique_id != nullptr)
+    return fail(MOE_ERR_INVALID_ARG, "nccl_unique_id must be NULL if tp_size == 1");
   if (!w->gate || !w->expert_blob) return fail(MOE_ERR_INVALID_ARG, "NULL weight table");
   for (int l = 0; l < L; ++l)
     if (!w->gate[l]) return fail(MOE_ERR_INVALID_ARG, "NULL gate pointer");
@@ -580,7 +587,7 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
     if (getenv("MOE_DEBUG_FETCH_LOG"))
       fprintf(stderr, "[moe init] cuStreamWriteValue32 %s\n", c->write_value32 ? "available" : "MISSING");
   }
-  if (P > 1) {
+  if (P > 1 && desc->nccl_unique_id) {
     std::string why;
     if (!nccl_load(&why)) return bail(fail(MOE_ERR_NCCL, why));
     ncclUniqueId id;
@@ -644,6 +651,9 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   if (c->fetch_stream) cudaStreamDestroy(c->fetch_stream);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(c->d_xchg);
+  cudaFree(c->d_ypart);
   cudaGetLastError();
   delete c;
   return MOE_OK;
@@ -781,6 +791,9 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   if (!x || !y) return fail(MOE_ERR_INVALID_ARG, "NULL x or y");
   if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(MOE_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
   if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
+  const bool tpf = c->P > 1 && c->tp_fused && c->fused;  // y summed in the kernel's epilogue (f3)
+  if (c->P > 1 && !tpf && !c->comm)
+    return fail(MOE_ERR_STATE, "tp_size > 1 without an NCCL communicator needs moe_tp_connect_* (fused path)");
   // host-side back-pressure: never let the GPU overwrite an unconsumed mailbox entry
   const unsigned long long seq = c->issued.load() + 1;
   while (seq - c->consumed.load(std::memory_order_acquire) >= (unsigned long long)kMailRing - 1)
@@ -817,7 +830,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ea.x = (const uint16_t*)x;
   ea.d = c->d; ea.ffr = c->ffr; ea.K = c->K;
   ea.h = c->d_h;
-  ea.y = y;
+  ea.y = tpf ? c->d_ypart : y;
   ea.ready = c->d_ready;
   ea.last_seq = c->d_last;
   ea.seq = seq;
@@ -842,6 +855,11 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
     fa.sts = ra.sts;
+    fa.tpP = tpf ? c->P : 0;
+    fa.tp_rank = c->rank;
+    fa.tp_calls = c->tp_calls;
+    for (int p = 0; p < 8; ++p) fa.peer[p] = tpf && p < c->P ? c->tp_peer[p] : nullptr;
+    fa.yout = y;
     prof_begin(c, 1, s, &pe);
     cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl, c->coop);
     if (e != cudaSuccess && c->pdl) {  // PDL not accepted: retry without it
@@ -852,6 +870,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     prof_end(c, s, &pe);
     if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("expert_fused launch: ") + cudaGetErrorString(e));
     c->fused_calls += 1;
+    if (tpf) c->tp_calls += 1;
     c->issued.store(seq, std::memory_order_release);  // the fetch thread may now wait for it
   } else {
     prof_begin(c, 0, s, &pe);
@@ -868,7 +887,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   }
   c->tokens[layer] += 1;
   c->trace_count += c->K;
-  if (c->P > 1) {
+  if (c->P > 1 && !tpf) {
     prof_begin(c, 3, s, &pe);
     ncclResult_t r = g_nccl.AllReduce(y, y, (size_t)c->d, ncclFloat32, ncclSum, c->comm, s);
     prof_end(c, s, &pe);
@@ -895,6 +914,8 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
       c->ffr % 128 || c->policy == MOE_POLICY_STATIC_RANDOM)
     return fail(MOE_ERR_UNSUPPORTED,
                 "prefill needs ways == n, a covered layer, MOE_MISS_FETCH, LRU/FIFO, K <= 2, d % 64 == 0, (ff/P) % 128 == 0");
+  if (c->P > 1 && !c->comm)
+    return fail(MOE_ERR_UNSUPPORTED, "prefill with tp_size > 1 reduces y with NCCL: create the ctx with nccl_unique_id");
   if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1064,6 +1085,168 @@ MOE_API moe_status moe_get_runtime_info(moe_ctx* c, moe_runtime_info* out) {
   out->ring_stages = c->fused ? c->plan.NS : 0;
   out->stage_bytes = c->fused ? c->plan.SB : 0;
   out->grid = c->fused ? c->fused_grid : 0;
+  out->tp_reduce = c->P == 1 ? 0 : (c->tp_fused && c->fused) ? 2 : c->comm ? 1 : 0;
+  return MOE_OK;
+}
+
+// ------------------------------------------------------------ fused TP reduction (f3)
+static moe_status tp_ensure_buffer(moe_ctx* c) {
+  if (c->d_xchg) return MOE_OK;
+  const long long bytes = tp_xchg_bytes(c->P, c->d);
+  cudaError_t e = cudaMalloc(&c->d_xchg, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_ypart, sizeof(float) * c->d);
+  if (e == cudaSuccess) e = cudaMemset(c->d_xchg, 0, (size_t)bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(c->d_xchg);
+    cudaFree(c->d_ypart);
+    c->d_xchg = nullptr;
+    c->d_ypart = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? MOE_ERR_OUT_OF_MEMORY : MOE_ERR_CUDA,
+                std::string("exchange buffer: ") + cudaGetErrorString(e));
+  }
+  return MOE_OK;
+}
+
+static moe_status tp_check(moe_ctx* c) {
+  if (c->P == 1) return fail(MOE_ERR_STATE, "tp_size == 1: nothing to reduce");
+  if (!c->fused) return fail(MOE_ERR_UNSUPPORTED, "the fused TP reduction needs the fused decode kernel (K <= 2)");
+  return MOE_OK;
+}
+
+// Zero this rank's counters and restart its call count: every rank must connect before any
+// rank's first call (multi-process: a barrier after moe_tp_connect_ipc).
+static moe_status tp_reset(moe_ctx* c) {
+  moe_status st = drain(c);
+  if (st != MOE_OK) return st;
+  CUDA_TRY(cudaMemset(c->d_xchg, 0, kTpSlotOff));
+  // the fused kernel's monotonic per-call counters assume a fixed grid: restart them (the
+  // grid may have changed in moe_tp_connect_local)
+  CUDA_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
+  CUDA_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * 2 * kMaxK));
+  CUDA_TRY(cudaDeviceSynchronize());
+  c->fused_calls = 0;
+  c->tp_calls = 0;
+  c->tp_fused = true;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_tp_exchange_buffer(moe_ctx* c, moe_tp_exchange* out) {
+  if (!c || !out) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  moe_status st = tp_check(c);
+  if (st != MOE_OK) return st;
+  DeviceGuard g(c->device);
+  st = tp_ensure_buffer(c);
+  if (st != MOE_OK) return st;
+  memset(out, 0, sizeof(*out));
+  out->dev_ptr = c->d_xchg;
+  out->bytes = tp_xchg_bytes(c->P, c->d);
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->d_xchg));
+  memcpy(out->ipc_handle, &h, 64);
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_tp_connect_ipc(moe_ctx* c, const uint8_t* handles) {
+  if (!c || !handles) return fail(MOE_ERR_INVALID_ARG, "NULL argument");
+  moe_status st = tp_check(c);
+  if (st != MOE_OK) return st;
+  DeviceGuard g(c->device);
+  st = tp_ensure_buffer(c);
+  if (st != MOE_OK) return st;
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  c->tp_fused = false;
+  for (int p = 0; p < c->P; ++p) {
+    if (p == c->rank) {
+      c->tp_peer[p] = c->d_xchg;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * p, 64);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+      c->ipc_opened.clear();
+      return fail(MOE_ERR_CUDA, "cudaIpcOpenMemHandle(rank " + std::to_string(p) + "): " + cudaGetErrorString(e));
+    }
+    c->ipc_opened.push_back(ptr);
+    c->tp_peer[p] = (uint8_t*)ptr;
+  }
+  return tp_reset(c);
+}
+
+MOE_API moe_status moe_tp_disconnect(moe_ctx* c) {
+  if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
+  DeviceGuard g(c->device);
+  moe_status st = drain(c);
+  if (st != MOE_OK) return st;
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  for (auto& p : c->tp_peer) p = nullptr;
+  c->tp_fused = false;
+  return MOE_OK;
+}
+
+MOE_API moe_status moe_tp_connect_local(moe_ctx* const* ctxs, int32_t P) {
+  if (!ctxs || P < 2 || P > 8) return fail(MOE_ERR_INVALID_ARG, "need 2 <= P <= 8 contexts");
+  moe_ctx* by_rank[8] = {};
+  for (int i = 0; i < P; ++i) {
+    moe_ctx* c = ctxs[i];
+    if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL context");
+    if (c->P != P) return fail(MOE_ERR_INVALID_ARG, "every context must have tp_size == P");
+    if (by_rank[c->rank]) return fail(MOE_ERR_INVALID_ARG, "tp_rank must be a permutation of 0..P-1");
+    by_rank[c->rank] = c;
+    if (c->L != ctxs[0]->L || c->d != ctxs[0]->d || c->ff != ctxs[0]->ff || c->n != ctxs[0]->n ||
+        c->K != ctxs[0]->K)
+      return fail(MOE_ERR_INVALID_ARG, "contexts of one TP group must share the model shape");
+    moe_status st = tp_check(c);
+    if (st != MOE_OK) return st;
+  }
+  for (int r = 0; r < P; ++r) {
+    DeviceGuard g(by_rank[r]->device);
+    moe_status st = tp_ensure_buffer(by_rank[r]);
+    if (st != MOE_OK) return st;
+  }
+  for (int r = 0; r < P; ++r) {
+    moe_ctx* c = by_rank[r];
+    DeviceGuard g(c->device);
+    int same = 0;
+    for (int q = 0; q < P; ++q) {
+      moe_ctx* o = by_rank[q];
+      c->tp_peer[q] = o->d_xchg;
+      if (o->device == c->device) {
+        ++same;
+        continue;
+      }
+      int can = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&can, c->device, o->device));
+      if (!can) return fail(MOE_ERR_UNSUPPORTED, "no peer access between devices of the TP group");
+      cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+    }
+    if (same > 1) {
+      // ranks sharing this GPU wait on each other inside their kernels: split the SMs so all
+      // of their grids are co-resident, and launch each call only after the previous one of
+      // the same rank has completed (no PDL early start, no cooperative launch)
+      FusedPlan plan;
+      const int grid = c->num_sms / same;
+      if (!plan_fused(c->d, c->ffr, c->n, c->K, grid, &plan))
+        return fail(MOE_ERR_UNSUPPORTED, "fused plan does not fit the per-rank grid");
+      c->fused_grid = grid;
+      c->pdl = false;
+      c->coop = false;
+    }
+  }
+  for (int r = 0; r < P; ++r) {
+    DeviceGuard g(by_rank[r]->device);
+    moe_status st = tp_reset(by_rank[r]);
+    if (st != MOE_OK) return st;
+  }
   return MOE_OK;
 }
 

@@ -81,3 +81,69 @@ def test_ff_slice_validation():
     assert tp.ff_slice(16384, 8, 7) == (14336, 16384)
     with pytest.raises(ValueError):
         tp.ff_slice(100, 4, 0)
+
+
+class _FakeMoe:
+    """Stands in for a TP context: records the handles tp.connect_peers hands it."""
+
+    def __init__(self, rank, world, fail=False):
+        self.tp_size, self.tp_rank = world, rank
+        self.got = None
+        self.fail = fail
+        self.disconnected = False
+
+    def tp_exchange_buffer(self):
+        return {"dev_ptr": 0, "bytes": 0, "ipc_handle": bytes([self.tp_rank + 1]) * 64}
+
+    def tp_connect_ipc(self, handles):
+        self.got = handles
+        if self.fail:
+            raise RuntimeError("no P2P")
+
+    def tp_disconnect(self):
+        self.disconnected = True
+
+
+def _connect_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2512_16473_b200 import tp
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = _FakeMoe(rank, world)
+        ok = tp.connect_peers(m)
+        bad = _FakeMoe((rank + 1) % world, world)
+        try:
+            tp.connect_peers(bad)
+            mismatch = False
+        except ValueError:
+            mismatch = True
+        # rank 1 cannot open its peers: every rank must fall back together
+        f = _FakeMoe(rank, world, fail=(rank == 1))
+        why = tp.connect_peers(f)
+        q.put((rank, m.got, mismatch, ok, why, f.disconnected))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_tp_connect_gathers_ipc_handles_in_rank_order():
+    """f3 host logic (world_size 2, gloo): every rank receives all ranks' 64-byte exchange
+    handles in rank order and a context whose rank disagrees with the group is refused."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_connect_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [bytes([r + 1]) * 64 for r in range(world)]
+    for rank, got, mismatch, ok, why, disconnected in res:
+        assert got == want and mismatch and ok == "fused-peer"
+        assert why == "rank 1: no P2P"
+        assert disconnected == (rank == 0)   # the rank that did connect reverts
