@@ -45,6 +45,7 @@ constexpr int kRouteBar = 13;              // named barrier: partial logits -> r
 constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
 constexpr int kTsPerCta = 40;             // debug timestamps per CTA (MOE_DEBUG_TS)
+constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stage
 
 // Packed fp32 FMA (sm_100: FFMA2): acc.{x,y} += a.{x,y} * b.{x,y}
 __device__ __forceinline__ float2 ffma2(const float2 a, const float2 b, const float2 c) {
@@ -210,7 +211,7 @@ __device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct)
 }
 
 // Shared memory: ring[NS][SB] | xh | full[NS] empty[NS] hbar | meta[NS] | part[NS][4] |
-//                parB[NS/2]
+//                parB[NS/2] | metaN[NS] | partB[NS/2][kMaxRB][4]
 //  - phase A: stage s (16 KB) = one W1 row + one W3 row, consumed by warps 2s, 2s+1 (one
 //    half of the row each); x lives in xh as fp32.
 //  - phase B: stages (2u, 2u+1) form one super-stage holding a whole W2 row (<= 2*SB),
@@ -247,6 +248,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   volatile int* meta = reinterpret_cast<volatile int*>(hbar + 1);
   volatile float* part = reinterpret_cast<volatile float*>(meta + NS);   // [NS][4]
   volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 4 * NS);  // full[2u] parity at phase B start
+  volatile int* metaN = reinterpret_cast<volatile int*>(parB + (NS >> 1));        // phase B: rows in the super-stage
+  volatile float* partB = reinterpret_cast<volatile float*>(metaN + NS);          // [NS/2][kMaxRB][4] row partials
+  const int RB = f.RB;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, d = a.d, ffr = a.ffr, n = f.r.n;
@@ -464,23 +468,26 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         const int r = sorder[si];
         const uint8_t* w2 = sbase[r] + w2off;
         unsigned* cB = ctr + kMaxFusedK + r;
-        auto issue_b = [&](int c) {
+        // RB consecutive W2 rows (contiguous in the slot) per super-stage: short rows
+        // (small ff_r) would otherwise leave too few bytes in flight per SM
+        auto issue_b = [&](int c, int nr) {
           const int s = 2 * (tb % NSB);
           acquire(s);
           meta[s] = c;
-          mbar_arrive_expect_tx(full + s, (uint32_t)rowB);
-          bulk_g2s(ring + (size_t)s * SB, w2 + (long long)c * rowB, (uint32_t)rowB, full + s, pol);
+          metaN[s] = nr;
+          mbar_arrive_expect_tx(full + s, (uint32_t)(nr * rowB));
+          bulk_g2s(ring + (size_t)s * SB, w2 + (long long)c * rowB, (uint32_t)(nr * rowB), full + s, pol);
           ++tb;
         };
         if (si > 0) marker_b(kSegB);
-        unsigned c1 = atomicAdd(cB, (unsigned)kChunkB);
-        for (int c = sbk.s0; c < sbk.s1; ++c) issue_b(c);
-        unsigned c2 = atomicAdd(cB, (unsigned)kChunkB);
+        unsigned c1 = atomicAdd(cB, (unsigned)RB);
+        for (int c = sbk.s0; c < sbk.s1; c += RB) issue_b(c, min(RB, sbk.s1 - c));
+        unsigned c2 = atomicAdd(cB, (unsigned)RB);
         while (sbk.tail0 + (int)c1 < d) {
-          const int r0 = sbk.tail0 + (int)c1, r1 = min(r0 + kChunkB, d);
+          const int r0 = sbk.tail0 + (int)c1, r1 = min(r0 + RB, d);
           c1 = c2;
-          if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(cB, (unsigned)kChunkB);
-          for (int c = r0; c < r1; ++c) issue_b(c);
+          if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(cB, (unsigned)RB);
+          issue_b(r0, r1 - r0);
         }
       }
       marker_b(kEnd);
@@ -600,17 +607,26 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           if (q == 0 && lane == 0) mbar_arrive(empty + s);
           break;
         }
-        float2 acc = make_float2(0.f, 0.f);
+        const int nr = metaN[s];           // rows c .. c+nr-1, contiguous in the stage
+        volatile float* pb = partB + u * kMaxRB * 4;
+        for (int i = 0; i < nr; ++i) {
+          const int4* wr = wv + i * nck;
+          float2 acc = make_float2(0.f, 0.f);
 #pragma unroll 4
-        for (int cc = k0 + lane; cc < k1; cc += 32) acc = dot8(wv[cc], hp0[cc], hp1[cc], acc);
-        const float sum = warp_sum(acc.x + acc.y);
-        if (lane == 0) part[4 * u + q] = sum;
-        named_bar_sync(2 + u, 128);        // the 4 quarters of this row are done
-        if (q == 0 && lane == 0) {
-          const float o = ((part[4 * u] + part[4 * u + 1]) + part[4 * u + 2]) + part[4 * u + 3];
-          mbar_arrive(empty + s);          // (partials read first: the next row rewrites them)
-          if (K == 1) a.y[c] = w * o;
-          else red_add_f32(a.y + c, w * o);  // K == 2: 0 + a + b is order-independent
+          for (int cc = k0 + lane; cc < k1; cc += 32) acc = dot8(wr[cc], hp0[cc], hp1[cc], acc);
+          const float sum = warp_sum(acc.x + acc.y);
+          if (lane == 0) pb[4 * i + q] = sum;
+        }
+        named_bar_sync(2 + u, 128);        // the 4 quarters of these rows are done
+        if (q == 0) {                      // lane i combines row i in a fixed order
+          float o = 0.f;
+          if (lane < nr) o = ((pb[4 * lane] + pb[4 * lane + 1]) + pb[4 * lane + 2]) + pb[4 * lane + 3];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);  // (partials read first: the next rows rewrite them)
+          if (lane < nr) {
+            if (K == 1) a.y[c + lane] = w * o;
+            else red_add_f32(a.y + c + lane, w * o);  // K == 2: 0 + a + b is order-independent
+          }
         }
       }
     }
@@ -673,7 +689,8 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
   if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
   const int xh = ((max(2 * d, ffr * 4) + 127) / 128) * 128;   // x (bf16) | one expert's h (fp32)
-  const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + 64;
+  const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + kMaxNS * 4 +
+                   (kMaxNS / 2) * kMaxRB * 16 + 64;
   int NS = (kFusedMaxDynSmem - xh - tail) / SB;
   if (NS > kMaxNS) NS = kMaxNS;
   NS &= ~1;                                      // stages pair into super-stages in phase B
@@ -687,6 +704,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->xh_bytes = xh;
   p->pctA = 88;
   p->pctB = 40;
+  p->RB = min(kMaxRB, (2 * SB) / (2 * ffr));     // W2 rows per phase-B super-stage
   p->smem = (size_t)NS * SB + xh + tail;
   p->threads = kThreadsF;
   return p->smem <= (size_t)kFusedMaxDynSmem;

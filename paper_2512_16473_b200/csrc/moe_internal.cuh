@@ -100,6 +100,7 @@ struct FusedArgs {
   int NS, SB;                     // ring stages / stage bytes
   int xh_bytes;
   int pctA, pctB;                 // share of phase A / B rows assigned statically (rest: stolen)
+  int RB;                         // W2 rows per phase-B super-stage
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
   unsigned long long* sts;        // this call's step record [kStsHead + 2*grid] (MOE_DEBUG_TS=1) or nullptr
@@ -116,7 +117,7 @@ struct FusedArgs {
 constexpr int kTpSlotOff = 256;
 inline long long tp_xchg_bytes(int P, int d) { return kTpSlotOff + 2ll * P * d * 4; }
 struct FusedPlan {
-  int SB, NS, xh_bytes, threads, pctA, pctB;
+  int SB, NS, xh_bytes, threads, pctA, pctB, RB;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

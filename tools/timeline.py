@@ -1,0 +1,83 @@
+#!/usr/bin/env python
+"""Per-CTA timeline of the fused decode kernel (MOE_DEBUG_TS=1, globaltimer ns).
+
+Runs `--steps` warm decode steps of one shape (bench_shapes.SHAPES) back to back, then
+reads the per-CTA phase marks of the LAST call (moe_debug_timestamps) and prints, for
+each mark, the median / min / max over CTAs relative to the END of the previous call
+(the latest CTA end of call seq-1, from moe_debug_step_ts): what the one-kernel step
+spends between the previous step's last byte and this step's first / last byte.
+
+    MOE_DEBUG_TS=1 python tools/timeline.py --shape mixtral-8x7b
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("MOE_DEBUG_TS", "1")
+
+import numpy as np  # noqa: E402
+
+import bench_shapes  # noqa: E402
+import harness  # noqa: E402
+import paper_2512_16473_b200 as moe  # noqa: E402
+
+# per-CTA slots written by expert_fused_kernel (kTsPerCta = 40)
+MARKS = {0: "cta_start", 8: "pdl_wait_done", 9: "x_landed", 10: "router_has_logits", 1: "route_published",
+         11: "route_decided", 2: "first_row_consumed", 3: "phase_A_done", 4: "phase_B_first_h", 6: "phase_B_second_h",
+         5: "cta_end"}
+KSTS_RING, KSTS_HEAD = 64, 8
+
+
+def main():
+    import torch
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="mixtral-8x7b")
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--tokens", type=int, default=64)
+    args = ap.parse_args()
+    d, ff, n, K = bench_shapes.SHAPES[args.shape]
+    hm = harness.host_model(1, d, ff, n, K)
+    x, _ = harness.hidden_states(hm, args.tokens, "uniform")
+    xd = torch.from_numpy(x.view(np.int16)).cuda()
+    yd = torch.empty((args.tokens, d), dtype=torch.float32, device="cuda")
+    lib = moe.lib()
+    lib.moe_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.moe_debug_step_ts.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    with harness.open_moe(hm) as m:
+        m.configure(ways=n, indexes=1, warm_start=True)
+        s = torch.cuda.Stream()
+        for i in range(args.steps):
+            m.forward(0, xd[i % args.tokens, 0].data_ptr(), yd[i % args.tokens].data_ptr(), s.cuda_stream)
+        s.synchronize()
+        G = m.runtime_info()["grid"]
+        ts = np.zeros(G * 40, np.uint64)
+        lib.moe_debug_timestamps(m._h.value, ts.ctypes.data)
+        stride = KSTS_HEAD + 2 * G
+        sts = np.zeros(KSTS_RING * stride, np.uint64)
+        lib.moe_debug_step_ts(m._h.value, sts.ctypes.data)
+    ts = ts.reshape(G, 40).astype(np.int64)
+    sts = sts.reshape(KSTS_RING, stride).astype(np.int64)
+    last = args.steps  # seq of the last call (seqs start at 1)
+    prev = sts[(last - 1) % KSTS_RING]
+    prev_end = int(prev[KSTS_HEAD + G:KSTS_HEAD + 2 * G].max())
+    cur = sts[last % KSTS_RING]
+    cur_end = int(cur[KSTS_HEAD + G:KSTS_HEAD + 2 * G].max())
+    out = {"shape": args.shape, "grid": G, "step_us_prev_end_to_end": (cur_end - prev_end) / 1e3, "marks_us": {}}
+    for slot, name in MARKS.items():
+        v = ts[:, slot]
+        v = v[v > 0] - prev_end
+        if v.size:
+            out["marks_us"][name] = {"median": statistics.median(v.tolist()) / 1e3, "min": float(v.min()) / 1e3,
+                                     "max": float(v.max()) / 1e3}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
