@@ -79,16 +79,6 @@ __device__ __forceinline__ float2 dot8_bf(const int4 w, const int4 x, float2 acc
   return acc;
 }
 
-// D(16x8, fp32) += A(16x16, bf16, row) * B(16x8, bf16, col): warp-level tensor-core MMA
-__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                               uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
 // bf16 pair (one 32-bit word) -> (lo, hi) fp32, exact
 __device__ __forceinline__ float2 bf2(uint32_t v) { return make_float2(bf_lo(v), bf_hi(v)); }
 
@@ -318,33 +308,31 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_wait(&xbar, 0);
     if (f.ts && threadIdx.x == 32) f.ts[b * kTsPerCta + 9] = globaltimer();
     if (pm && threadIdx.x == 32) pm[1] = clock64();
-    // Gate GEMV z = Wg x on the tensor cores: mma.sync m16n8k16 (bf16 in, fp32
-    // accumulate), A = 16 gate rows, B = x in every column; consumer warp w takes 16-wide
-    // k-steps [ks0, ks1). Per-warp partials, reduced in a fixed order by the router warp.
+    // Gate GEMV z = Wg x: a few KFLOP, latency-bound — spread over every consumer
+    // thread instead of a dependent chain of MMAs: thread i takes 16-B chunks i, i + nthr, ...
+    // of x and of 8 gate rows at a time (sm_100 mixed-precision FMAs, bf16 products exact
+    // in fp32), then a warp-shuffle tree per expert. Per-warp partials, reduced in a fixed
+    // order by the router warp (deterministic).
     mbar_wait(&gbar, 0);
+    if (pm && threadIdx.x == 32) pm[0] = clock64();
     {
-      const int g = lane >> 2, t = lane & 3;
-      const int ksteps = (d + 15) >> 4, kps = (ksteps + nwc - 1) / nwc;  // d % 16 == 8: half a last step
-      const int ks0 = cw * kps, ks1 = min(ksteps, ks0 + kps);
-      for (int e0 = 0; e0 < n; e0 += 16) {
-        const bool r0 = e0 + g < n, r1 = e0 + 8 + g < n;
-        const uint8_t* A0 = ring + (size_t)(e0 + g) * gstride;
-        const uint8_t* A1 = ring + (size_t)(e0 + 8 + g) * gstride;
-        float c[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int ks = ks0; ks < ks1; ++ks) {
-          const int kb = (ks * 16 + 2 * t) * 2;   // byte offset of this thread's k pair
-          const bool hi = ks * 16 + 8 < d;         // upper 8 columns of the step inside the row
-          const uint32_t a0 = r0 ? *reinterpret_cast<const uint32_t*>(A0 + kb) : 0u;
-          const uint32_t a2 = r0 && hi ? *reinterpret_cast<const uint32_t*>(A0 + kb + 16) : 0u;
-          const uint32_t a1 = r1 ? *reinterpret_cast<const uint32_t*>(A1 + kb) : 0u;
-          const uint32_t a3 = r1 && hi ? *reinterpret_cast<const uint32_t*>(A1 + kb + 16) : 0u;
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xh + kb);
-          const uint32_t b1 = hi ? *reinterpret_cast<const uint32_t*>(xh + kb + 16) : 0u;
-          mma_bf16_16816(c, a0, a1, a2, a3, b0, b1);
+      const int nch = d >> 3;                       // 16-B chunks per row
+      const int4* xq = reinterpret_cast<const int4*>(xh);
+      for (int e0 = 0; e0 < n; e0 += 8) {
+        float2 acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = make_float2(0.f, 0.f);
+        for (int ch = ctid; ch < nch; ch += nthr) {
+          const int4 xv = xq[ch];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (e0 + j < n)
+              acc[j] = dot8_bf(reinterpret_cast<const int4*>(ring + (size_t)(e0 + j) * gstride)[ch], xv, acc[j]);
         }
-        if (t == 0) {
-          if (r0) zpart[cw * n + e0 + g] = c[0];
-          if (r1) zpart[cw * n + e0 + 8 + g] = c[2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float z = warp_sum(acc[j].x + acc[j].y);
+          if (lane == 0 && e0 + j < n) zpart[cw * n + e0 + j] = z;
         }
       }
     }
@@ -354,6 +342,18 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // ---------------------------------------------------------------- router warp
     // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects.
     // The producer starts as soon as the slots are known (all hit: before the bookkeeping).
+    // While the consumers run the gate GEMV: where each expert sits in the set (lane e:
+    // its way and that way's generation, from the pre-access directory), so an all-hit
+    // route can be published straight from the logits.
+    const bool fast = ra.covered && ra.miss_mode == MOE_MISS_FETCH;
+    int way_of = -1;
+    uint32_t gen_of = 0u;
+    if (fast)
+      for (int w = 0; w < ra.M; ++w) {
+        const int t = __shfl_sync(0xffffffffu, ds.tag, w);
+        const uint32_t g = __shfl_sync(0xffffffffu, ds.gen, w);
+        if (t == lane) { way_of = w; gen_of = g; }
+      }
     named_bar_sync(kRouteBar, nthr + 32);
     if (f.ts && lane == 0) f.ts[b * kTsPerCta + 10] = globaltimer();
     if (pm && lane == 0) pm[3] = clock64();
@@ -361,7 +361,34 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (lane < n)
       for (int w = 0; w < nwc; ++w) z += zpart[w * n + lane];  // fixed order
     bool published = false;
+    if (fast) {
+      // all-hit fast path: rank of expert `lane` by (z desc, index asc) — the same order
+      // route_decide derives from the same z — and, if all K selected experts are resident,
+      // their slots in rank order (a hit never changes its way's generation; FETCH: no wait)
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const float zj = __shfl_sync(0xffffffffu, z, j);
+        rank += (zj > z) || (zj == z && j < lane);
+      }
+      const bool sel = lane < n && rank < K;
+      if (__popc(__ballot_sync(0xffffffffu, sel && way_of >= 0)) == K) {
+        if (sel) {
+          const int slot = ra.slot_base + way_of;
+          sslot[rank] = slot;
+          sgen[rank] = gen_of;
+          swait[rank] = 0;
+          shost[rank] = 0;
+          sbase[rank] = a.pool + (long long)slot * a.slot_bytes;
+          sorder[rank] = rank;
+        }
+        if (lane == 0) snseg = K;
+        mbar_arrive(&rbar);                // release (each lane its own writes): route published
+        if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
+        published = true;
+      }
+    }
     auto publish = [&](const LaneRoute& lr) {
+      if (published) return;               // (already published by the fast path)
       if (lane < K) {
         sslot[lane] = lr.slot;
         sgen[lane] = lr.gen;

@@ -76,6 +76,20 @@ def main():
         if v.size:
             out["marks_us"][name] = {"median": statistics.median(v.tolist()) / 1e3, "min": float(v.min()) / 1e3,
                                      "max": float(v.max()) / 1e3}
+    # SM-clock marks inside the routing prologue (clock64, same CTA): 24 gate rows in smem
+    # (consumer warp 0, after x), 25 x landed (consumer
+    # warp 0), 26 its gate GEMV done, 27 router warp past the logits barrier, 28 top-K done,
+    # 29 probe done (all-hit publish), 30 LRU bookkeeping done, 31 decision returned
+    names = {24: "gate_rows_landed", 25: "x_landed", 26: "gemv_done", 27: "router_has_logits", 28: "topk_done", 29: "probe_published",
+             30: "lru_done", 31: "decided"}
+    base = ts[:, 27]
+    cyc = {}
+    for slot, name in names.items():
+        v = ts[:, slot]
+        ok = (v > 0) & (base > 0)
+        if ok.any():
+            cyc[name] = statistics.median((v[ok] - base[ok]).tolist())
+    out["router_cycles_rel_logits"] = cyc
     print(json.dumps(out, indent=1))
 
 
