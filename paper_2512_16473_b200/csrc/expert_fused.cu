@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     f.ts[b * kTsPerCta + 0] = globaltimer();
     f.ts[b * kTsPerCta + 6] = 0;
     f.ts[b * kTsPerCta + 7] = 0;
+    f.ts[b * kTsPerCta + 15] = 0;
+    f.ts[b * kTsPerCta + 16] = 0;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -478,6 +480,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
         marker_a(kSegA - r);  // every stage publishes its rows of h_r
       }
+      if (f.ts) f.ts[b * kTsPerCta + 12] = globaltimer();  // last phase-A row issued
       marker_a(kEnd);
       // phase B: whole W2 rows into super-stages (2u, 2u+1); W2 does not depend on h, so
       // these loads stream while the consumers finish phase A and load h
@@ -506,7 +509,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           bulk_g2s(ring + (size_t)s * SB, w2 + (long long)c * rowB, (uint32_t)(nr * rowB), full + s, pol);
           ++tb;
         };
-        if (si > 0) marker_b(kSegB);
+        if (si > 0) {
+          if (f.ts) f.ts[b * kTsPerCta + 13] = globaltimer();  // last B_o0 row issued
+          marker_b(kSegB);
+        }
         unsigned c1 = atomicAdd(cB, (unsigned)RB);
         for (int c = sbk.s0; c < sbk.s1; c += RB) issue_b(c, min(RB, sbk.s1 - c));
         unsigned c2 = atomicAdd(cB, (unsigned)RB);
@@ -517,6 +523,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           issue_b(r0, r1 - r0);
         }
       }
+      if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
       marker_b(kEnd);
       // publish the call's progress to the host fetch thread (PCIe write overlaps the tail);
       // the system fence orders this call's mailbox entry (written by the routing warp
@@ -593,6 +600,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     named_bar_sync(1, nthr);
     if (cw == 0 && lane == 0) {
       const unsigned long long* bar = f.bar + 16 * r;
+      const bool dbg = f.ts && f.ts[b * kTsPerCta + 16] == 0;
+      if (dbg) f.ts[b * kTsPerCta + 16] = globaltimer();  // first h load: CTA out of phase A
       if (ld_acquire_u64(bar) < bar_target) {
         const unsigned long long t0 = globaltimer();
         while (ld_acquire_u64(bar) < bar_target) {
@@ -600,6 +609,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
         }
       }
+      if (dbg) f.ts[b * kTsPerCta + 17] = globaltimer();  // first h published grid-wide
       asm volatile("fence.proxy.async.global;" ::: "memory");
       mbar_arrive_expect_tx(hbar, (uint32_t)ffr * 4u);
       bulk_g2s(xh, a.h + (long long)r * ffr, (uint32_t)ffr * 4u, hbar, policy_evict_first());
@@ -629,6 +639,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         mbar_wait(full + s, ph);
         ph ^= 1;
         const int c = meta[s];
+        if (f.ts && cw == 0 && lane == 0 && !f.ts[b * kTsPerCta + 15]) f.ts[b * kTsPerCta + 15] = globaltimer();
         if (c < 0) {                       // kSegB (next expert) or kEnd
           named_bar_sync(2 + u, 128);
           if (q == 0 && lane == 0) mbar_arrive(empty + s);
