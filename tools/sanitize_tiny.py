@@ -1,3 +1,4 @@
+import os, sys; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, harness, inputs, oracle, sys
 import paper_2512_16473_b200 as moe
 c = inputs.CONFIGS["tiny"]
@@ -12,3 +13,12 @@ for mode in (moe.MISS_FETCH, moe.MISS_HOST_COMPUTE):
     ok = all(np.array_equal(tr[f].astype(int), ref.records[f].astype(int)) for f in ("expert", "hit", "way", "evicted"))
     err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()) for t in range(6) for l in range(4))
     print("mode", mode, "bitexact", ok, "err", err, flush=True)
+# all-hit fast publish path: every expert resident (M = n, warm)
+ref = oracle.decode(x, hm.gates, lambda l, e: inputs.expert_weights(l, e, hm.d, hm.ff), N=4, M=8, K=2, warm_start=True)
+with harness.open_moe(hm) as m:
+    m.configure(ways=8, indexes=4, warm_start=True)
+    y = harness.run_decode(m, x)
+    tr = m.trace()
+ok = all(np.array_equal(tr[f].astype(int), ref.records[f].astype(int)) for f in ("expert", "hit", "way", "evicted"))
+err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()) for t in range(6) for l in range(4))
+print("warm all-hit bitexact", ok, "err", err, flush=True)
