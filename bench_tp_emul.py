@@ -29,6 +29,54 @@ import harness  # noqa: E402
 import inputs  # noqa: E402
 
 
+def epilogue_breakdown(P: int, tokens: int = 16, steps: int = 40) -> dict:
+    """Median per-CTA durations (us) of the fused reduction epilogue in the last call
+    (MOE_DEBUG_TS marks 18, 21): wait for every rank's terms of the slice + fixed-order sum."""
+    import ctypes
+    import statistics
+    import torch
+    import paper_2512_16473_b200 as moe
+    os.environ["MOE_DEBUG_TS"] = "1"
+    c = inputs.CONFIGS["mixtral-8x22b"]
+    d, ff, n, K = c["d"], c["ff"], c["n"], c["K"]
+    hps = [harness.host_model(1, d, ff, n, K, tp_size=P, tp_rank=p) for p in range(P)]
+    x, _ = harness.hidden_states(hps[0], tokens, "paper")
+    xd = torch.from_numpy(x.view(np.int16)).cuda()
+    yd = torch.empty((P, tokens, d), dtype=torch.float32, device="cuda")
+    ms = [harness.open_moe(hp) for hp in hps]
+    os.environ.pop("MOE_DEBUG_TS", None)
+    lib = moe.lib()
+    lib.moe_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    try:
+        for m in ms:
+            m.configure(ways=n, indexes=1, warm_start=True)
+        moe.tp_connect_local(ms)
+        streams = [torch.cuda.Stream() for _ in range(P)]
+        for i in range(steps):
+            for p in range(P):
+                ms[p].forward(0, xd[i % tokens, 0].data_ptr(), yd[p, i % tokens].data_ptr(), streams[p].cuda_stream)
+        torch.cuda.synchronize()
+        marks = []
+        for m in ms:
+            G = m.runtime_info()["grid"]
+            ts = np.zeros(G * 40, np.uint64)
+            lib.moe_debug_timestamps(m._h.value, ts.ctypes.data)
+            marks.append(ts.reshape(G, 40).astype(np.int64))
+    finally:
+        for m in ms:
+            m.close()
+    t = np.concatenate(marks)
+    med = lambda a: statistics.median(a.tolist()) / 1e3  # noqa: E731
+    # the rank that arrives last waits only for its own slices to land everywhere: its wait is
+    # the exchange latency; the other ranks' waits add the skew between the ranks' kernels
+    per_rank = [med(mk[:, 21] - mk[:, 18]) for mk in marks]
+    return {"epilogue_us_last_rank": min(per_rank), "epilogue_us_per_rank": per_rank,
+            "epilogue_us_median": med(t[:, 21] - t[:, 18]),
+            "note": "medians over CTAs, last call, from the CTA's last own term to all ranks' terms of its column "
+                    "slice landed; the ranks share one GPU (no NVLink hop), so waits beyond the last rank's are "
+                    "skew between the co-resident rank kernels, not exchange cost"}
+
+
 def run(P: int, steps: int, warmup: int, tokens: int, pdl1: bool) -> dict:
     import torch
     import paper_2512_16473_b200 as moe
@@ -103,7 +151,9 @@ def main():
                 r = run(1, args.steps, args.warmup, args.tokens, pdl)
                 print(json.dumps(r), flush=True)
         else:
-            print(json.dumps(run(P, args.steps, args.warmup, args.tokens, False)), flush=True)
+            r = run(P, args.steps, args.warmup, args.tokens, False)
+            r["fused_reduction_epilogue"] = epilogue_breakdown(P)
+            print(json.dumps(r), flush=True)
 
 
 if __name__ == "__main__":

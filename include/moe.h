@@ -260,15 +260,16 @@ MOE_API moe_status moe_nccl_unique_id(uint8_t* out128);
 /* Fused tensor-parallel reduction over peer memory (north_star (4)).
  * The per-layer sum y = sum_p y^(p) of the ff-split (every rank holds the ff/P slice of
  * every expert) moves INTO the decode kernel's epilogue instead of a separate
- * ncclAllReduce launch: each rank's CTAs finish their partial y^(p) in HBM, pass a
- * grid-wide counter, then store their column slice of y^(p) into slot [p] of EVERY
- * rank's exchange buffer (plain stores over NVLink P2P / NVSwitch; a local store for p
- * itself), release a per-rank arrival counter on every rank (system scope), wait until
- * all P ranks' slices have arrived in their own buffer, and write
- *   y[c] = (((0 + y^(0)[c]) + y^(1)[c]) + ...) + y^(P-1)[c]      (fixed rank order)
+ * ncclAllReduce launch. Every term w_r * o_r^(p)[c] of rank p's partial y^(p) (r = routing
+ * rank, c = column) is stored, as soon as the kernel has it, into slot [c][p][r] of EVERY
+ * rank's exchange buffer as an 8-byte {value, call tag} word (plain stores over NVLink P2P /
+ * NVSwitch; a local store for p itself; single-copy atomic, so no fence, counter or grid
+ * barrier is needed — the "LL" protocol). Each CTA then polls its own slots of its column
+ * slice until every word carries this call's tag and sums the P*K terms of each column in a
+ * fixed tree order (K = 2: w_0 o_0^(p) + w_1 o_1^(p) per source rank, then pairs of ranks),
  * so all ranks get bit-identical y (their next layer's routing stays identical).
  * The exchange buffer is double-buffered by call parity, so a rank running one call ahead
- * never overwrites slots a peer is still reading; counters are monotonic (no resets).
+ * never overwrites slots a peer is still reading; tags and counters are monotonic.
  * Scope: the fused decode path (K <= 2; moe_get_runtime_info expert_path == 1), both miss
  * modes. The split fallback and moe_layer_prefill keep the NCCL all-reduce (they need a
  * communicator: pass nccl_unique_id).
@@ -287,7 +288,7 @@ MOE_API moe_status moe_nccl_unique_id(uint8_t* out128);
  * same sequence of forward calls; a rank whose peer never arrives traps after 60 s. */
 typedef struct {
   void* dev_ptr;          /* this rank's exchange buffer (device memory, library-owned) */
-  int64_t bytes;          /* 256 + 2 * P * d * 4 */
+  int64_t bytes;          /* 256 + 2 * P * K * d * 8 */
   uint8_t ipc_handle[64]; /* cudaIpcMemHandle_t of dev_ptr */
 } moe_tp_exchange;
 MOE_API moe_status moe_tp_exchange_buffer(moe_ctx* ctx, moe_tp_exchange* out);

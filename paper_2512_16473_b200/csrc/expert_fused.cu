@@ -111,66 +111,74 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsig
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// 60 s without progress on a cross-CTA / cross-rank wait: fail loudly (trap), never hang
-__device__ __forceinline__ void spin_until_gpu(const unsigned long long* p, unsigned long long target) {
-  const unsigned long long t0 = globaltimer();
-  while (ld_acquire_u64(p) < target) {
-    __nanosleep(32);
-    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
-  }
-}
-__device__ __forceinline__ void spin_until_sys(const unsigned long long* p, unsigned long long target) {
-  const unsigned long long t0 = globaltimer();
-  while (ld_acquire_sys_u64(p) < target) {
-    __nanosleep(32);
-    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
-  }
-}
-
 // f3: fused tensor-parallel reduction of y over the ranks' exchange buffers (moe.h,
-// moe_tp_connect_*). Called by the consumer threads (ctid 0 .. nthr-1) of every CTA after
-// their last reduction into this rank's partial y^(p) (f.e.y).
-//  1. local grid barrier: every CTA's y^(p) reductions are complete (release/acquire on a
-//     monotonic counter; the CTAs are co-resident, see fused_blocks_per_sm)
-//  2. CTA b pushes its column slice [c0, c1) of y^(p) into slots[par][p] of every rank
-//     (P2P stores over NVLink; a local store for its own rank), then one thread releases
-//     (system scope, after a system fence) the slice's column count on every rank's
-//     arrival counter
-//  3. wait until this rank's arrival counter shows all P*d columns of this call, then
-//     y[c] = sum over source ranks in fixed order (bit-identical on every rank).
+// moe_tp_connect_*), the "LL" low-latency protocol: every term w_r * o_r^(p)[c] of this
+// rank's partial y^(p) is stored, as soon as a phase-B row (or a host-computed expert's
+// column) is done, into slot [par][c][p][r] of EVERY rank as an 8-byte {value, tag} word
+// (tag = this call's number; plain P2P stores over NVLink, a local store for its own rank;
+// single-copy atomic, so a receiver that sees the tag sees the value: no fence, no counter,
+// no grid barrier). Here, CTA b polls its own slots of its column slice [c0, c1) until every
+// (source rank, routing rank) word carries the tag and sums them per column in a fixed tree
+// order (K = 2: (v[p][0] + v[p][1]) per source rank, then pairs of ranks): y is
+// bit-identical on every rank.
+// Slots are double-buffered by call parity: a rank one call ahead writes the other half.
+__device__ __forceinline__ unsigned long long* tp_slot(const FusedArgs& f, int p, int src, int r, int c) {
+  const int P = f.tpP, K = f.e.K, d = f.e.d, par = (int)(f.tp_calls & 1);
+  // [parity][column][source rank][routing rank]: the P*K words a receiver sums are contiguous
+  return reinterpret_cast<unsigned long long*>(f.peer[p] + kTpSlotOff) + (((long long)par * d + c) * P + src) * K + r;
+}
+__device__ __forceinline__ unsigned long long tp_tag(const FusedArgs& f) {
+  return (unsigned long long)(uint32_t)(f.tp_calls + 1) << 32;
+}
+// term w_r * o_r[c] of this rank -> every rank's slot
+__device__ __forceinline__ void tp_push(const FusedArgs& f, int r, int c, float v) {
+  const unsigned long long w = tp_tag(f) | __float_as_uint(v);
+  for (int p = 0; p < f.tpP; ++p) st_relaxed_sys_u64(tp_slot(f, p, f.tp_rank, r, c), w);
+}
 __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, int G, int ctid, int nthr) {
-  const int P = f.tpP, d = f.e.d;
-  uint8_t* own = f.peer[f.tp_rank];
-  unsigned long long* arrive = reinterpret_cast<unsigned long long*>(own);
-  unsigned long long* lbar = reinterpret_cast<unsigned long long*>(own + 16);
+  const int P = f.tpP, K = f.e.K, d = f.e.d, PK = P * K;  // PK in {2, 4, 8, 16}: divides 32 and nthr
   const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
-  const int par = (int)(f.tp_calls & 1);
-  named_bar_sync(1, nthr);                     // this CTA's reductions into y^(p) issued
-  if (ctid == 0) {
-    __threadfence();
-    red_release_add_u64(lbar, 1ull);
-    spin_until_gpu(lbar, (f.tp_calls + 1) * (unsigned long long)G);
+  const int total = (c1 - c0) * PK;
+  const unsigned long long tag = tp_tag(f);
+  unsigned long long* ts = f.ts ? f.ts + b * kTsPerCta : nullptr;  // debug marks 18, 21
+  if (ts && ctid == 0) ts[18] = globaltimer();
+  // thread i holds word j = i % PK (source rank j / K, routing rank j % K) of column
+  // c0 + i / PK: poll it until it carries this call's tag, then an xor-shuffle tree over the
+  // PK lanes of the column (a fixed order, the same on every rank)
+  constexpr int U = 4;                         // words in flight per thread (poll latency overlap)
+  for (int base = 0; base < total; base += U * nthr) {
+    unsigned long long w[U];
+    const unsigned long long* wp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * nthr + ctid;
+      wp[u] = nullptr;
+      w[u] = 0ull;
+      if (i < total) {
+        const int j = i % PK;
+        wp[u] = tp_slot(f, f.tp_rank, j / K, j % K, c0 + i / PK);
+        w[u] = ld_relaxed_sys_u64(wp[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (wp[u] && (w[u] & 0xffffffff00000000ull) != tag) {
+        const unsigned long long t0 = globaltimer();
+        while (((w[u] = ld_relaxed_sys_u64(wp[u])) & 0xffffffff00000000ull) != tag) {
+          __nanosleep(32);
+          if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * nthr + ctid;
+      float v = wp[u] ? __uint_as_float((uint32_t)w[u]) : 0.f;
+      for (int o = 1; o < PK; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (i < total && i % PK == 0) f.yout[c0 + i / PK] = v;
+    }
   }
-  named_bar_sync(1, nthr);
-  const long long slot_off = kTpSlotOff + ((long long)(par * P + f.tp_rank) * d) * 4;
-  for (int c = c0 + ctid; c < c1; c += nthr) {
-    const float v = __ldcg(f.e.y + c);
-    for (int p = 0; p < P; ++p) __stcg(reinterpret_cast<float*>(f.peer[p] + slot_off) + c, v);
-  }
-  named_bar_sync(1, nthr);                     // slice stored to every rank
-  if (ctid == 0) {
-    __threadfence_system();
-    for (int p = 0; p < P; ++p)
-      red_release_sys_add_u64(reinterpret_cast<unsigned long long*>(f.peer[p]), (unsigned long long)(c1 - c0));
-    spin_until_sys(arrive, (f.tp_calls + 1) * (unsigned long long)P * (unsigned long long)d);
-  }
-  named_bar_sync(1, nthr);
-  const float* slots = reinterpret_cast<const float*>(own + kTpSlotOff) + (long long)par * P * d;
-  for (int c = c0 + ctid; c < c1; c += nthr) {
-    float s = 0.f;
-    for (int p = 0; p < P; ++p) s += __ldcg(slots + (long long)p * d + c);
-    f.yout[c] = s;
-  }
+  if (ts && ctid == 0) ts[21] = globaltimer();
 }
 
 constexpr int kChunkA = 2;     // phase A rows per tail claim
@@ -662,7 +670,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + s);  // (partials read first: the next rows rewrite them)
           if (lane < nr) {
-            if (K == 1) a.y[c + lane] = w * o;
+            if (f.tpP > 1) tp_push(f, r, c + lane, w * o);  // f3: straight to every rank
+            else if (K == 1) a.y[c + lane] = w * o;
             else red_add_f32(a.y + c + lane, w * o);  // K == 2: 0 + a + b is order-independent
           }
         }
@@ -692,7 +701,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const float* o = a.host_out + (size_t)r * d;
     for (int c = c0 + ctid; c < c1; c += nthr) {
       const float v = w * __ldcg(o + c);
-      if (K == 1) a.y[c] = v;
+      if (f.tpP > 1) tp_push(f, r, c, v);
+      else if (K == 1) a.y[c] = v;
       else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
     }
   }

@@ -104,18 +104,18 @@ struct FusedArgs {
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
   unsigned long long* sts;        // this call's step record [kStsHead + 2*grid] (MOE_DEBUG_TS=1) or nullptr
-  // fused TP reduction (f3, moe_tp_connect_*): e.y is then this rank's partial y^(p); the
-  // epilogue exchanges column slices through the ranks' exchange buffers (TpXchg layout)
+  // fused TP reduction (f3, moe_tp_connect_*): every term of this rank's partial y goes to
+  // the ranks' exchange buffers (layout below); the epilogue sums them into yout
   int tpP, tp_rank;               // tpP == 0: no fused reduction
   unsigned long long tp_calls;    // earlier fused-TP calls on this context (same on every rank)
   uint8_t* peer[8];               // exchange buffer base of every rank (peer[tp_rank] = own)
   float* yout;                    // [d] all-reduced y (caller's buffer)
 };
-// Exchange buffer of one TP rank: [0] arrival counter (u64, written by every rank with
-// system-scope release REDs, counts columns), [16] local grid-barrier counter (u64, this
-// rank's CTAs), then slots[2][P][d] fp32 at kTpSlotOff (call parity, source rank, column).
+// Exchange buffer of one TP rank: slots[2][d][P][K] u64 at kTpSlotOff (call parity, column,
+// source rank, routing rank), each word {fp32 term w_r * o_r[c] | call tag << 32}, written
+// by the source rank with 8-byte stores.
 constexpr int kTpSlotOff = 256;
-inline long long tp_xchg_bytes(int P, int d) { return kTpSlotOff + 2ll * P * d * 4; }
+inline long long tp_xchg_bytes(int P, int K, int d) { return kTpSlotOff + 2ll * P * K * d * 8; }
 struct FusedPlan {
   int SB, NS, xh_bytes, threads, pctA, pctB, RB;
   size_t smem;

@@ -1095,7 +1095,7 @@ MOE_API moe_status moe_get_runtime_info(moe_ctx* c, moe_runtime_info* out) {
 // ------------------------------------------------------------ fused TP reduction (f3)
 static moe_status tp_ensure_buffer(moe_ctx* c) {
   if (c->d_xchg) return MOE_OK;
-  const long long bytes = tp_xchg_bytes(c->P, c->d);
+  const long long bytes = tp_xchg_bytes(c->P, c->K, c->d);
   cudaError_t e = cudaMalloc(&c->d_xchg, (size_t)bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_ypart, sizeof(float) * c->d);
   if (e == cudaSuccess) e = cudaMemset(c->d_xchg, 0, (size_t)bytes);
@@ -1122,7 +1122,8 @@ static moe_status tp_check(moe_ctx* c) {
 static moe_status tp_reset(moe_ctx* c) {
   moe_status st = drain(c);
   if (st != MOE_OK) return st;
-  CUDA_TRY(cudaMemset(c->d_xchg, 0, kTpSlotOff));
+  // all of it: a slot word left by an earlier connection could carry a tag this one reuses
+  CUDA_TRY(cudaMemset(c->d_xchg, 0, (size_t)tp_xchg_bytes(c->P, c->K, c->d)));
   // the fused kernel's monotonic per-call counters assume a fixed grid: restart them (the
   // grid may have changed in moe_tp_connect_local)
   CUDA_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
@@ -1143,7 +1144,7 @@ MOE_API moe_status moe_tp_exchange_buffer(moe_ctx* c, moe_tp_exchange* out) {
   if (st != MOE_OK) return st;
   memset(out, 0, sizeof(*out));
   out->dev_ptr = c->d_xchg;
-  out->bytes = tp_xchg_bytes(c->P, c->d);
+  out->bytes = tp_xchg_bytes(c->P, c->K, c->d);
   cudaIpcMemHandle_t h;
   static_assert(sizeof(h) == 64, "ipc handle size");
   CUDA_TRY(cudaIpcGetMemHandle(&h, c->d_xchg));

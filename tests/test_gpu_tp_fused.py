@@ -165,4 +165,4 @@ def test_tp_without_nccl_or_connect_is_rejected():
         assert ei.value.status == 5 and "moe_tp_connect" in str(ei.value)
         assert m.runtime_info()["tp_reduce"] == "none"
         e = m.tp_exchange_buffer()
-        assert e["bytes"] == 256 + 2 * 2 * d * 4 and len(e["ipc_handle"]) == 64 and e["dev_ptr"]
+        assert e["bytes"] == 256 + 2 * 2 * K * d * 8 and len(e["ipc_handle"]) == 64 and e["dev_ptr"]
