@@ -231,10 +231,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ float swgt[kMaxFusedK];
   __shared__ int swait[kMaxFusedK], shost[kMaxFusedK], sslot[kMaxFusedK], sorder[kMaxFusedK];
   __shared__ uint32_t sgen[kMaxFusedK];
-  __shared__ int snseg;
+  __shared__ int snseg, smerged;
   __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
   __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
   __shared__ __align__(8) uint64_t gbar, xbar, rbar, wbar;  // gate rows / x landed; slots / weights published
+  __shared__ __align__(8) uint64_t hbarK[kMaxFusedK];     // merged phase B: h_r landed (router warp's copy)
+  __shared__ volatile int pairA[kMaxNS / 2];               // merged phase B: pair u's even stage left phase A
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
@@ -287,6 +289,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(&xbar, 1);
     mbar_init(&rbar, 32);  // every router lane arrives after its own shared-memory writes
     mbar_init(&wbar, 32);
+    for (int r = 0; r < kMaxFusedK; ++r) mbar_init(hbarK + r, 1);
+    for (int u = 0; u < kMaxNS / 2; ++u) pairA[u] = 0;
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
     const uint64_t pl = policy_evict_last();
@@ -391,7 +395,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           sbase[rank] = a.pool + (long long)slot * a.slot_bytes;
           sorder[rank] = rank;
         }
-        if (lane == 0) snseg = K;
+        if (lane == 0) {
+          snseg = K;
+          smerged = f.merge && K == kMaxFusedK;  // every expert resident and ready
+        }
         mbar_arrive(&rbar);                // release (each lane its own writes): route published
         if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
         published = true;
@@ -413,7 +420,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       const unsigned below = (1u << lane) - 1u;
       if (lane < K && !lr.host)
         sorder[lr.wait ? __popc(dev_ready) + __popc(dev_wait & below) : __popc(dev_ready & below)] = lane;
-      if (lane == 0) snseg = __popc(dev_ready | dev_wait);
+      if (lane == 0) {
+        snseg = __popc(dev_ready | dev_wait);
+        smerged = f.merge && K == kMaxFusedK && __popc(dev_ready) == K;
+      }
       mbar_arrive(&rbar);                  // release (each lane its own writes): route published
       if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
       published = true;
@@ -433,6 +443,23 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       ra.mail->seq = ra.seq;
     }
     griddep_launch_dependents();
+    if (smerged && lane == 0) {
+      // merged phase B: bring every expert's h into its own buffer as soon as it is published
+      // grid-wide (the buffers lie past x: no phase-A reader is disturbed)
+      for (int si = 0; si < K; ++si) {
+        const int r = sorder[si];
+        const unsigned long long* bar = f.bar + 16 * r;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_u64(bar) < bar_target) {
+          __nanosleep(64);
+          if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_arrive_expect_tx(hbarK + r, (uint32_t)ffr * 4u);
+        bulk_g2s(xh + f.hoff + (size_t)r * f.hstride, a.h + (long long)r * ffr, (uint32_t)ffr * 4u, hbarK + r,
+                 policy_evict_first());
+      }
+    }
     return;
   }
 
@@ -501,6 +528,43 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           mbar_arrive(full + s);
         }
       };
+      if (smerged) {
+        // Merged phase B (every expert resident and ready, every h resident in shared
+        // memory, loaded by the router warp as soon as it is published): the experts' W2 rows
+        // in turn with the same static-then-steal schedule, but no marker between experts
+        // (no ring drain) and no CTA-wide h reload: every chunk's meta carries its expert and
+        // a warp waits for that expert's h the first time it meets it.
+        const RowSched sbk = make_sched(d, b, G, f.pctB);
+        auto issue_b = [&](int r, int c, int nr) {
+          const int s = 2 * (tb % NSB);
+          acquire(s);
+          meta[s] = (r << 24) | c;
+          metaN[s] = nr;
+          mbar_arrive_expect_tx(full + s, (uint32_t)(nr * rowB));
+          bulk_g2s(ring + (size_t)s * SB, sbase[r] + w2off + (long long)c * rowB, (uint32_t)(nr * rowB), full + s, pol);
+          ++tb;
+        };
+        for (int si = 0; si < nseg; ++si) {     // experts in turn, without markers between them
+          const int r = sorder[si];
+          unsigned* cB = ctr + kMaxFusedK + r;
+          unsigned e1 = atomicAdd(cB, (unsigned)RB);
+          for (int c = sbk.s0; c < sbk.s1; c += RB) issue_b(r, c, min(RB, sbk.s1 - c));
+          unsigned e2 = atomicAdd(cB, (unsigned)RB);
+          while (sbk.tail0 + (int)e1 < d) {
+            const int r0 = sbk.tail0 + (int)e1, r1 = min(r0 + RB, d);
+            e1 = e2;
+            if (sbk.tail0 + (int)e1 < d) e2 = atomicAdd(cB, (unsigned)RB);
+            issue_b(r, r0, r1 - r0);
+          }
+        }
+        if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
+        marker_b(kEnd);
+        if (b == 0) {
+          __threadfence_system();
+          *a.last_seq = a.seq;
+        }
+        return;
+      }
       const RowSched sbk = make_sched(d, b, G, f.pctB);
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
@@ -511,7 +575,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         auto issue_b = [&](int c, int nr) {
           const int s = 2 * (tb % NSB);
           acquire(s);
-          meta[s] = c;
+          meta[s] = (r << 24) | c;
           metaN[s] = nr;
           mbar_arrive_expect_tx(full + s, (uint32_t)(nr * rowB));
           bulk_g2s(ring + (size_t)s * SB, w2 + (long long)c * rowB, (uint32_t)(nr * rowB), full + s, pol);
@@ -596,7 +660,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
     named_bar_sync(2 + sA, 64);
     if (half == 0 && lane == 0) mbar_arrive(empty + sA);  // release the end marker's stage
-    if (half == 0 && lane == 0 && (sA & 1) == 0) parB[sA >> 1] = ph;  // full[sA] parity for phase B
+    if (half == 0 && lane == 0 && (sA & 1) == 0) {
+      parB[sA >> 1] = ph;                  // full[sA] parity for phase B
+      __threadfence_block();
+      pairA[sA >> 1] = 1;                  // (merged phase B starts without a CTA barrier)
+    }
   }
   if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 3] = globaltimer();
   // h_r -> shared memory (xh) before phase-B segment r: every consumer is done with xh,
@@ -604,7 +672,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   // (the async proxy reads global memory written through the generic proxy by other CTAs:
   // fence the proxies first).
   uint32_t hph = 0;
-  auto load_h = [&](int r) {
+  auto load_h = [&](int r, bool) {
     named_bar_sync(1, nthr);
     if (cw == 0 && lane == 0) {
       const unsigned long long* bar = f.bar + 16 * r;
@@ -626,6 +694,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     hph ^= 1;
   };
   const int nseg = snseg;                  // (visible: published before the producer's first marker)
+  const bool mm = smerged;                 // merged phase B: one pass over every expert
   mbar_wait(&wbar, 0);                     // gate weights (long published by now)
   {
     const int u = cw >> 2, q = cw & 3;     // super-stage and quarter of the W2 row
@@ -633,26 +702,45 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const int s = 2 * u;
     const int nck = rowB >> 4;
     const int k0 = (nck * q) >> 2, k1 = (nck * (q + 1)) >> 2;
-    const float4* hp0 = reinterpret_cast<const float4*>(xh);   // h[8c .. 8c+3]
-    const float4* hp1 = hp0 + (ffr >> 3);                      // h[8c+4 .. 8c+7]
     const int4* wv = reinterpret_cast<const int4*>(ring + (size_t)s * SB);
-    for (int si = 0; si < nseg; ++si) {
-      const int r = sorder[si];
-      const float w = swgt[r];
-      load_h(r);
-      if (si == 0 && active) ph = parB[u];  // written before load_h's barrier
+    // pair u's named barrier: its even stage's phase-A id (that stage has left phase A by the
+    // time any of the pair's warps uses it: no mixed 64/128-thread use of one id)
+    const int bid = 2 + 2 * u;
+    uint32_t seen = 0u;                    // merged: experts whose h this warp has waited for
+    for (int si = 0; si < (mm ? 1 : nseg); ++si) {
+      if (mm) {                            // no CTA barrier: start once the pair's even stage is out
+        if (active) {
+          if (lane == 0)
+            while (!pairA[u]) {
+            }
+          __syncwarp();
+          ph = parB[u];
+        }
+      } else {
+        load_h(sorder[si], false);
+        if (si == 0 && active) ph = parB[u];  // written before load_h's barrier
+      }
       if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + (si == 0 ? 4 : 6)] = globaltimer();
       if (!active) continue;
       while (true) {
         mbar_wait(full + s, ph);
         ph ^= 1;
-        const int c = meta[s];
+        const int m = meta[s];
         if (f.ts && cw == 0 && lane == 0 && !f.ts[b * kTsPerCta + 15]) f.ts[b * kTsPerCta + 15] = globaltimer();
-        if (c < 0) {                       // kSegB (next expert) or kEnd
-          named_bar_sync(2 + u, 128);
+        if (m < 0) {                       // kSegB (next expert) or kEnd
+          named_bar_sync(bid, 128);
           if (q == 0 && lane == 0) mbar_arrive(empty + s);
           break;
         }
+        const int r = m >> 24, c = m & 0xFFFFFF;  // expert (routing rank), first row
+        const float w = swgt[r];
+        if (mm && !((seen >> r) & 1u)) {   // merged: h_r copied in by the router warp
+          mbar_wait(hbarK + r, 0);
+          seen |= 1u << r;
+        }
+        // h_r[8k .. 8k+3] / h_r[8k+4 .. 8k+7] (2-plane layout)
+        const float4* hp0 = reinterpret_cast<const float4*>(xh + (mm ? f.hoff + (size_t)r * f.hstride : 0));
+        const float4* hp1 = hp0 + (ffr >> 3);
         const int nr = metaN[s];           // rows c .. c+nr-1, contiguous in the stage
         volatile float* pb = partB + u * kMaxRB * 4;
         for (int i = 0; i < nr; ++i) {
@@ -663,7 +751,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           const float sum = warp_sum(acc.x + acc.y);
           if (lane == 0) pb[4 * i + q] = sum;
         }
-        named_bar_sync(2 + u, 128);        // the 4 quarters of these rows are done
+        named_bar_sync(bid, 128);          // the 4 quarters of these rows are done
         if (q == 0) {                      // lane i combines row i in a fixed order
           float o = 0.f;
           if (lane < nr) o = ((pb[4 * lane] + pb[4 * lane + 1]) + pb[4 * lane + 2]) + pb[4 * lane + 3];
@@ -736,12 +824,20 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   if (K > 2 || grid < K) return false;          // deterministic combine needs K <= 2
   const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
   if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
-  const int xh = ((max(2 * d, ffr * 4) + 127) / 128) * 128;   // x (bf16) | one expert's h (fp32)
   const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + kMaxNS * 4 +
                    (kMaxNS / 2) * kMaxRB * 16 + 64;
-  int NS = (kFusedMaxDynSmem - xh - tail) / SB;
-  if (NS > kMaxNS) NS = kMaxNS;
-  NS &= ~1;                                      // stages pair into super-stages in phase B
+  const int xh1 = ((max(2 * d, ffr * 4) + 127) / 128) * 128;  // x (bf16) | one expert's h (fp32)
+  const int hoff = ((2 * d + 127) / 128) * 128, hstride = ((ffr * 4 + 127) / 128) * 128;
+  const int xh2 = hoff + K * hstride;            // x | every expert's own h buffer (merged phase B)
+  auto stages = [&](int xh) {
+    int ns = (kFusedMaxDynSmem - xh - tail) / SB;
+    if (ns > kMaxNS) ns = kMaxNS;
+    return ns & ~1;                              // stages pair into super-stages in phase B
+  };
+  // merged phase B when holding every expert's h costs no ring stage (small ff_r)
+  const bool merge = K == kMaxFusedK && stages(xh2) == stages(xh1);
+  const int xh = merge ? xh2 : xh1;
+  const int NS = stages(xh);
   if (NS < 4) return false;
   // the gate rows and x are staged in the (still empty) ring before the route is known
   const long long gate = (2ll * d + 16) * n;                            // staged in the ring
@@ -753,6 +849,9 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->pctA = 88;
   p->pctB = 40;
   p->RB = min(kMaxRB, (2 * SB) / (2 * ffr));     // W2 rows per phase-B super-stage
+  p->merge = merge ? 1 : 0;
+  p->hoff = hoff;
+  p->hstride = hstride;
   p->smem = (size_t)NS * SB + xh + tail;
   p->threads = kThreadsF;
   return p->smem <= (size_t)kFusedMaxDynSmem;

@@ -559,6 +559,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       const char* pb = getenv("MOE_STATIC_B");
       if (pa && atoi(pa) >= 0 && atoi(pa) <= 100) c->plan.pctA = atoi(pa);
       if (pb && atoi(pb) >= 0 && atoi(pb) <= 100) c->plan.pctB = atoi(pb);
+      const char* mg = getenv("MOE_MERGE");   // merged phases (default: when the plan allows)
+      if (mg && mg[0] == '0') c->plan.merge = 0;
       const char* rb = getenv("MOE_ROWS_B");  // W2 rows per phase-B super-stage (<= plan's)
       if (rb && atoi(rb) >= 1 && atoi(rb) < c->plan.RB) c->plan.RB = atoi(rb);
     }
@@ -574,8 +576,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       INIT_TRY(cudaMemset(c->d_sts, 0, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
     }
     if (getenv("MOE_DEBUG_KERNEL") || getenv("MOE_DEBUG_TS")) {
-      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d RB=%d xh=%d smem=%zu grid=%d\n", (int)c->fused, c->plan.NS,
-              c->plan.SB, c->plan.RB, c->plan.xh_bytes, c->plan.smem, c->fused_grid);
+      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d RB=%d merge=%d xh=%d smem=%zu grid=%d\n", (int)c->fused,
+              c->plan.NS, c->plan.SB, c->plan.RB, c->plan.merge, c->plan.xh_bytes, c->plan.smem, c->fused_grid);
   }
   }
   {
@@ -855,6 +857,9 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.pctA = c->plan.pctA;
     fa.pctB = c->plan.pctB;
     fa.RB = c->plan.RB;
+    fa.merge = c->plan.merge;
+    fa.hoff = c->plan.hoff;
+    fa.hstride = c->plan.hstride;
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
     fa.sts = ra.sts;
