@@ -209,7 +209,7 @@ __device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct)
 }
 
 // Shared memory: ring[NS][SB] | xh | full[NS] empty[NS] hbar | meta[NS] | part[NS][4] |
-//                parB[NS/2] | metaN[NS] | partB[NS/2][kMaxRB][4]
+//                parB[NS/2] | metaN[NS] | partB[NS/2][2][kMaxRB][4]
 //  - phase A: stage s (16 KB) = one W1 row + one W3 row, consumed by warps 2s, 2s+1 (one
 //    half of the row each); x lives in xh as fp32.
 //  - phase B: stages (2u, 2u+1) form one super-stage holding a whole W2 row (<= 2*SB),
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
   __shared__ __align__(8) uint64_t gbar, xbar, rbar, wbar;  // gate rows / x landed; slots / weights published
   __shared__ __align__(8) uint64_t hbarK[kMaxFusedK];     // merged phase B: h_r landed (router warp's copy)
-  __shared__ volatile int pairA[kMaxNS / 2];               // merged phase B: pair u's even stage left phase A
+  __shared__ __align__(8) uint64_t pairbar[kMaxNS / 2];  // merged phase B: pair u's even stage left phase A
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
   const int NS = f.NS, SB = f.SB, NSB = NS >> 1;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   volatile float* part = reinterpret_cast<volatile float*>(meta + NS);   // [NS][4]
   volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 4 * NS);  // full[2u] parity at phase B start
   volatile int* metaN = reinterpret_cast<volatile int*>(parB + (NS >> 1));        // phase B: rows in the super-stage
-  volatile float* partB = reinterpret_cast<volatile float*>(metaN + NS);          // [NS/2][kMaxRB][4] row partials
+  volatile float* partB = reinterpret_cast<volatile float*>(metaN + NS);          // [NS/2][2][kMaxRB][4] row partials
   const int RB = f.RB;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(&rbar, 32);  // every router lane arrives after its own shared-memory writes
     mbar_init(&wbar, 32);
     for (int r = 0; r < kMaxFusedK; ++r) mbar_init(hbarK + r, 1);
-    for (int u = 0; u < kMaxNS / 2; ++u) pairA[u] = 0;
+    for (int u = 0; u < kMaxNS / 2; ++u) mbar_init(pairbar + u, 1);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
     const uint64_t pl = policy_evict_last();
@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       ra.mail->seq = ra.seq;
     }
     griddep_launch_dependents();
-    if (smerged && lane == 0) {
+    __syncwarp();                          // (sorder / smerged written by other router lanes)
+    if (lane == 0 && smerged) {
       // merged phase B: bring every expert's h into its own buffer as soon as it is published
       // grid-wide (the buffers lie past x: no phase-A reader is disturbed)
       for (int si = 0; si < K; ++si) {
@@ -662,8 +663,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (half == 0 && lane == 0) mbar_arrive(empty + sA);  // release the end marker's stage
     if (half == 0 && lane == 0 && (sA & 1) == 0) {
       parB[sA >> 1] = ph;                  // full[sA] parity for phase B
-      __threadfence_block();
-      pairA[sA >> 1] = 1;                  // (merged phase B starts without a CTA barrier)
+      mbar_arrive(pairbar + (sA >> 1));    // (release; merged phase B starts without a CTA barrier)
     }
   }
   if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 3] = globaltimer();
@@ -707,13 +707,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // time any of the pair's warps uses it: no mixed 64/128-thread use of one id)
     const int bid = 2 + 2 * u;
     uint32_t seen = 0u;                    // merged: experts whose h this warp has waited for
+    uint32_t nchunk = 0u;                  // chunks this pair has processed
     for (int si = 0; si < (mm ? 1 : nseg); ++si) {
       if (mm) {                            // no CTA barrier: start once the pair's even stage is out
         if (active) {
-          if (lane == 0)
-            while (!pairA[u]) {
-            }
-          __syncwarp();
+          mbar_wait(pairbar + u, 0);
           ph = parB[u];
         }
       } else {
@@ -742,7 +740,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         const float4* hp0 = reinterpret_cast<const float4*>(xh + (mm ? f.hoff + (size_t)r * f.hstride : 0));
         const float4* hp1 = hp0 + (ffr >> 3);
         const int nr = metaN[s];           // rows c .. c+nr-1, contiguous in the stage
-        volatile float* pb = partB + u * kMaxRB * 4;
+        // partials double-buffered by chunk parity: the next chunk's writes go to the other
+        // buffer, so every write-after-read is ordered by a named barrier
+        volatile float* pb = partB + (u * 2 + (nchunk++ & 1)) * kMaxRB * 4;
         for (int i = 0; i < nr; ++i) {
           const int4* wr = wv + i * nck;
           float2 acc = make_float2(0.f, 0.f);
@@ -825,7 +825,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
   if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
   const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + kMaxNS * 4 +
-                   (kMaxNS / 2) * kMaxRB * 16 + 64;
+                   (kMaxNS / 2) * 2 * kMaxRB * 16 + 64;
   const int xh1 = ((max(2 * d, ffr * 4) + 127) / 128) * 128;  // x (bf16) | one expert's h (fp32)
   const int hoff = ((2 * d + 127) / 128) * 128, hstride = ((ffr * 4 + 127) / 128) * 128;
   const int xh2 = hoff + K * hstride;            // x | every expert's own h buffer (merged phase B)
