@@ -21,15 +21,21 @@ using namespace tc;
 
 constexpr int kThreadsTC = 192;
 
-template <int BN, int NB>
+// MT m-tiles per CTA tile share every B (weight) tile: operand bytes per FLOP drop by
+// (1 + NB*BN/BM) / (MT + NB*BN/BM) — the GEMMs are bound by the TMA / L2 -> SM stream
+// (~6.3 KB/cycle chip-wide), not by the tensor cores, at MT = 1.
+template <int BN, int NB, int MT>
 struct TcCfg {
   static constexpr int kA = BM * BK * 2;          // 16 KB
   static constexpr int kB = BN * BK * 2;          // 16 / 32 KB
-  static constexpr int kStage = kA + NB * kB;
+  static constexpr int kStage = MT * kA + NB * kB;
   static constexpr int kStages = (kFusedMaxDynSmem - 2048) / kStage > 6 ? 6 : (kFusedMaxDynSmem - 2048) / kStage;
   static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
-  // two accumulator buffers (double-buffered epilogue)
-  static constexpr int kTmemCols = 2 * NB * BN <= 32 ? 32 : 2 * NB * BN <= 64 ? 64 : 2 * NB * BN <= 128 ? 128 : 2 * NB * BN <= 256 ? 256 : 512;
+  static constexpr int kAcc = MT * NB * BN;       // TMEM columns of one accumulator set
+  static constexpr int kBufs = 2 * kAcc <= 512 ? 2 : 1;  // double-buffered epilogue when it fits
+  static constexpr int kTmemCols = kBufs * kAcc <= 32 ? 32 : kBufs * kAcc <= 64 ? 64 : kBufs * kAcc <= 128 ? 128
+                                 : kBufs * kAcc <= 256 ? 256 : 512;
+  static_assert(kAcc <= 512, "accumulators exceed TMEM");
 };
 
 struct TileCoord {
@@ -39,6 +45,7 @@ struct TileCoord {
   int out_row;    // output row base (H_g row / y gather row / C row)
   int out_col;    // output column base
   int valid;
+  int nm;         // valid m-tiles in the group (prefill: the last group of a block may be short)
 };
 
 // Tile enumeration (persistent CTAs take tiles id = blockIdx.x + i * gridDim.x):
@@ -46,16 +53,22 @@ struct TileCoord {
 //  prefill: expert block, then n tile, then m tile (fastest) — the CTAs working on the m
 //           tiles of one (expert, n tile) run concurrently, so each weight tile is read
 //           from HBM once and re-served from L2.
+template <int MT>
 __device__ __forceinline__ int num_tiles(const TcArgs& p, int BN) {
   const int ntn = (p.N + BN - 1) / BN;
   if (p.mode == TC_MODE_PLAIN) return ntn * ((p.M + BM - 1) / BM);
-  return ntn * p.plan->total_mtiles;
+  int n = 0;
+  for (int blk = 0; blk < p.plan->nblk; ++blk)
+    n += ntn * ((p.plan->mt_pref[blk + 1] - p.plan->mt_pref[blk] + MT - 1) / MT);
+  return n;
 }
 
+template <int MT>
 __device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN, int id) {
   TileCoord t;
   t.valid = 1;
   t.blk = 0;
+  t.nm = 1;
   const int ntn = (p.N + BN - 1) / BN;
   if (p.mode == TC_MODE_PLAIN) {
     const int ntm = (p.M + BM - 1) / BM;
@@ -68,15 +81,22 @@ __device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN, int id) {
     return t;
   }
   const PrefillPlan* pl = p.plan;
-  // expert block of this tile: blocks own ntn * mtiles(blk) consecutive tile ids
-  int blk = 0;
-  while (blk + 1 < pl->nblk && pl->mt_pref[blk + 1] * ntn <= id) ++blk;
-  const int local = id - pl->mt_pref[blk] * ntn;
-  const int mtiles = pl->mt_pref[blk + 1] - pl->mt_pref[blk];
-  const int nt = local / mtiles, mt = local - nt * mtiles;
-  const int row = pl->row_off[blk] + mt * BM;
+  // expert block of this tile: blocks own ntn * groups(blk) consecutive tile ids, a group
+  // being MT consecutive m-tiles of the block
+  int blk = 0, base = 0, mtiles = 0, ng = 0;
+  while (true) {
+    mtiles = pl->mt_pref[blk + 1] - pl->mt_pref[blk];
+    ng = (mtiles + MT - 1) / MT;
+    if (blk + 1 >= pl->nblk || id < base + ntn * ng) break;
+    base += ntn * ng;
+    ++blk;
+  }
+  const int local = id - base;
+  const int nt = local / ng, g = local - nt * ng;
+  const int row = pl->row_off[blk] + g * MT * BM;
   const long long slot = pl->slot[blk];
   t.blk = blk;
+  t.nm = min(MT, mtiles - g * MT);
   t.a_row = row;
   t.out_row = row;
   t.out_col = nt * BN;
@@ -91,12 +111,14 @@ __device__ __forceinline__ TileCoord tile_of(const TcArgs& p, int BN, int id) {
 }
 
 // Persistent, warp-specialised: warp 4 = TMA producer, warp 5 = MMA issuer (TMEM owner),
-// warps 0-3 = epilogue. Two accumulator buffers in TMEM: the epilogue of tile i overlaps
-// the main loop of tile i+1.
-template <int BN, int NB>
+// warps 0-3 = epilogue. A CTA tile is MT m-tiles x BN columns (x NB B operands); with two
+// accumulator sets in TMEM (when they fit) the epilogue of tile i overlaps the main loop of
+// tile i+1.
+template <int BN, int NB, int MT>
 __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_constant__ TcArgs p) {
-  using C = TcCfg<BN, NB>;
-  constexpr int kAcc = NB * BN;  // TMEM columns of one accumulator buffer
+  using C = TcCfg<BN, NB, MT>;
+  constexpr int kAcc = C::kAcc;  // TMEM columns of one accumulator set: [MT][NB][BN]
+  constexpr int kBufs = C::kBufs;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
@@ -106,7 +128,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = num_tiles(p, BN);
+  const int ntiles = num_tiles<MT>(p, BN);
   if ((int)blockIdx.x >= ntiles) return;
   const int ktiles = p.K / BK;
 
@@ -134,7 +156,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
       prefetch_tmap(&p.mapB);
       int it = 0;  // global k-block counter (ring position)
       for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
-        const TileCoord tc = tile_of(p, BN, id);
+        const TileCoord tc = tile_of<MT>(p, BN, id);
         if (p.mode != TC_MODE_PLAIN && p.plan->wait[tc.blk])  // expert filled by this call
           ptx::wait_ready(p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
         for (int kb = 0; kb < ktiles; ++kb, ++it) {
@@ -142,8 +164,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
           ptx::mbar_wait(empty + s, ((it / C::kStages) & 1) ^ 1);
           uint8_t* st = smem + (size_t)s * C::kStage;
           ptx::mbar_arrive_expect_tx(full + s, (uint32_t)C::kStage);
-          tma_load_2d(st, &p.mapA, kb * BK, tc.a_row, full + s);
-          for (int j = 0; j < NB; ++j) tma_load_2d(st + C::kA + j * C::kB, &p.mapB, kb * BK, tc.b_row[j], full + s);
+          // (a short group's extra A tile reads the following rows / TMA zero fill: unused)
+          for (int i = 0; i < MT; ++i) tma_load_2d(st + i * C::kA, &p.mapA, kb * BK, tc.a_row + i * BM, full + s);
+          for (int j = 0; j < NB; ++j)
+            tma_load_2d(st + MT * C::kA + j * C::kB, &p.mapB, kb * BK, tc.b_row[j], full + s);
         }
       }
     }
@@ -152,8 +176,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     const uint32_t idesc = umma_idesc_bf16(BM, BN);
     int it = 0, tl = 0;
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++tl) {
-      const int acc = tl & 1;
-      ptx::mbar_wait(tempty + acc, ((tl >> 1) & 1) ^ 1);   // epilogue drained this buffer
+      const int acc = tl % kBufs;
+      const int nm = tile_of<MT>(p, BN, id).nm;
+      ptx::mbar_wait(tempty + acc, ((tl / kBufs) & 1) ^ 1);   // epilogue drained this buffer
       tc_fence_after();
       const uint32_t tacc = tmem + acc * kAcc;
       for (int kb = 0; kb < ktiles; ++kb, ++it) {
@@ -162,13 +187,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
         tc_fence_after();
         if (lane == 0) {
           const uint8_t* st = smem + (size_t)s * C::kStage;
-          const uint64_t da = umma_desc_sw128(st);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k) {
 #pragma unroll
-            for (int j = 0; j < NB; ++j) {
-              const uint64_t db = umma_desc_sw128(st + C::kA + j * C::kB);
-              umma_bf16(tacc + j * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            for (int i = 0; i < MT; ++i) {
+              if (i >= nm) break;
+              const uint64_t da = umma_desc_sw128(st + i * C::kA);
+#pragma unroll
+              for (int j = 0; j < NB; ++j) {
+                const uint64_t db = umma_desc_sw128(st + MT * C::kA + j * C::kB);
+                umma_bf16(tacc + (i * NB + j) * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              }
             }
           }
           umma_commit(empty + s);             // stage free once these MMAs have read it
@@ -182,57 +211,58 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     const int row = warp * 32 + lane;                      // accumulator row = TMEM lane
     int tl = 0;
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++tl) {
-      const TileCoord tc = tile_of(p, BN, id);
-      const int acc = tl & 1;
-      ptx::mbar_wait(tfull + acc, (tl >> 1) & 1);
+      const TileCoord tc = tile_of<MT>(p, BN, id);
+      const int acc = tl % kBufs;
+      ptx::mbar_wait(tfull + acc, (tl / kBufs) & 1);
       tc_fence_after();
-      const uint32_t tbase = tmem + acc * kAcc + ((uint32_t)(warp * 32) << 16);
-      if (p.mode == TC_MODE_PLAIN) {
-        const int grow = tc.out_row + row;
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(tbase + c, v);
-          if (grow < p.M) {
-            float* dst = p.C + (size_t)grow * p.N + tc.out_col + c;
+      for (int i = 0; i < tc.nm; ++i) {
+        const uint32_t tbase = tmem + acc * kAcc + i * NB * BN + ((uint32_t)(warp * 32) << 16);
+        const int orow = tc.out_row + i * BM + row;
+        if (p.mode == TC_MODE_PLAIN) {
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + c, v);
+            if (orow < p.M) {
+              float* dst = p.C + (size_t)orow * p.N + tc.out_col + c;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (tc.out_col + c + i < p.N) dst[i] = __uint_as_float(v[i]);
+              for (int q = 0; q < 32; ++q)
+                if (tc.out_col + c + q < p.N) dst[q] = __uint_as_float(v[q]);
+            }
           }
-        }
-      } else if (p.mode == TC_MODE_SWIGLU) {
-        // h = silu(g) * u  (R4), rounded to bf16 for the second GEMM's A operand
-        const int grow = tc.out_row + row;
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t g[32], u[32];
-          tmem_ld32(tbase + c, g);
-          tmem_ld32(tbase + BN + c, u);
-          __nv_bfloat162 hv[16];
+        } else if (p.mode == TC_MODE_SWIGLU) {
+          // h = silu(g) * u  (R4), rounded to bf16 for the second GEMM's A operand
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t g[32], u[32];
+            tmem_ld32(tbase + c, g);
+            tmem_ld32(tbase + BN + c, u);
+            __nv_bfloat162 hv[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float g0 = __uint_as_float(g[i]), g1 = __uint_as_float(g[i + 1]);
-            const float h0 = g0 / (1.0f + __expf(-g0)) * __uint_as_float(u[i]);
-            const float h1 = g1 / (1.0f + __expf(-g1)) * __uint_as_float(u[i + 1]);
-            hv[i / 2] = __floats2bfloat162_rn(h0, h1);
+            for (int q = 0; q < 32; q += 2) {
+              const float g0 = __uint_as_float(g[q]), g1 = __uint_as_float(g[q + 1]);
+              const float h0 = g0 / (1.0f + __expf(-g0)) * __uint_as_float(u[q]);
+              const float h1 = g1 / (1.0f + __expf(-g1)) * __uint_as_float(u[q + 1]);
+              hv[q / 2] = __floats2bfloat162_rn(h0, h1);
+            }
+            __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.H + (size_t)orow * p.ldh + tc.out_col + c);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<const uint4*>(hv + q);
           }
-          __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.H + (size_t)grow * p.ldh + tc.out_col + c);
+        } else {
+          // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
+          const int tok = p.plan->tok[orow];
+          const float w = p.plan->wrow[orow];
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + c, v);
+            if (tok >= 0 && tc.out_col + c < p.N) {
+              float* dst = p.y + (size_t)tok * p.N + tc.out_col + c;
 #pragma unroll
-          for (int i = 0; i < 16; i += 4) *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(hv + i);
-        }
-      } else {
-        // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
-        const int tok = p.plan->tok[tc.out_row + row];
-        const float w = p.plan->wrow[tc.out_row + row];
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(tbase + c, v);
-          if (tok >= 0 && tc.out_col + c < p.N) {
-            float* dst = p.y + (size_t)tok * p.N + tc.out_col + c;
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
-                           "f"(w * __uint_as_float(v[i])), "f"(w * __uint_as_float(v[i + 1])),
-                           "f"(w * __uint_as_float(v[i + 2])), "f"(w * __uint_as_float(v[i + 3]))
-                           : "memory");
+              for (int q = 0; q < 32; q += 4)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + q),
+                             "f"(w * __uint_as_float(v[q])), "f"(w * __uint_as_float(v[q + 1])),
+                             "f"(w * __uint_as_float(v[q + 2])), "f"(w * __uint_as_float(v[q + 3]))
+                             : "memory");
+            }
           }
         }
       }
@@ -248,43 +278,51 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
   }
 }
 
-template <int BN, int NB>
+template <int BN, int NB, int MT>
 cudaError_t launch_tc(const TcArgs& p, int max_tiles, int num_sms, cudaStream_t s) {
-  using C = TcCfg<BN, NB>;
+  using C = TcCfg<BN, NB, MT>;
   const int grid = max_tiles < num_sms ? max_tiles : num_sms;
-  tc_gemm_kernel<BN, NB><<<grid, kThreadsTC, C::kSmem, s>>>(p);
+  tc_gemm_kernel<BN, NB, MT><<<grid, kThreadsTC, C::kSmem, s>>>(p);
   return cudaGetLastError();
 }
+
+template <int BN, int NB, int MT>
+cudaError_t preload_tc() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<BN, NB, MT>);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(tc_gemm_kernel<BN, NB, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TcCfg<BN, NB, MT>::kSmem);
+  return e;
+}
+
+constexpr int kMtPrefill = 2;  // m-tiles per CTA tile in the prefill GEMMs
 
 }  // namespace
 
 cudaError_t preload_tc_kernels() {
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<128, 1>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<128, 2>);
-  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, tc_gemm_kernel<256, 1>);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<128, 1>::kSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<128, 2>::kSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(tc_gemm_kernel<256, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256, 1>::kSmem);
+  cudaError_t e = preload_tc<128, 1, 1>();
+  if (e == cudaSuccess) e = preload_tc<128, 2, kMtPrefill>();
+  if (e == cudaSuccess) e = preload_tc<256, 1, kMtPrefill>();
   return e;
 }
 
 cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s) {  // C = A B^T, BN = 128
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return launch_tc<128, 1>(p, ((p.N + 127) / 128) * ((p.M + BM - 1) / BM), sms, s);
+  return launch_tc<128, 1, 1>(p, ((p.N + 127) / 128) * ((p.M + BM - 1) / BM), sms, s);
 }
 
 cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return launch_tc<128, 2>(p, ((p.N + 127) / 128) * max_mtiles, sms, s);
+  return launch_tc<128, 2, kMtPrefill>(p, ((p.N + 127) / 128) * max_mtiles, sms, s);
 }
 
 cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return launch_tc<256, 1>(p, ((p.N + 255) / 256) * max_mtiles, sms, s);
+  return launch_tc<256, 1, kMtPrefill>(p, ((p.N + 255) / 256) * max_mtiles, sms, s);
 }
 
 }  // namespace moe

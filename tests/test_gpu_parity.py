@@ -401,6 +401,38 @@ def test_prefill_tensor_core_path_tiny(tiny, warm, preset, policy):
     assert worst <= TOL, worst
 
 
+def test_prefill_tiny_multi_mtile_groups(tiny):
+    """Prompts long enough that experts own several 128-row m-tiles: the prefill GEMMs take
+    two m-tiles per CTA tile (full and short groups)."""
+    T = 600
+    x, _ = harness.hidden_states(tiny, T, "uniform")
+    ref = _oracle_run(tiny, x, N=tiny.L, M=tiny.n, warm=True)
+    y, tr, st = _prefill_run(tiny, x, tiny.n, True)
+    order = np.lexsort((tr["rank"], tr["layer"], tr["token"]))
+    for f in EXACT_FIELDS:
+        np.testing.assert_array_equal(tr[order][f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    worst = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
+                for t in range(T) for l in range(tiny.L))
+    assert worst <= TOL, worst
+
+
+@pytest.mark.slow
+def test_prefill_mixtral_layer_1024_tokens_sampled():
+    """BASELINE configs[1] layer, 1024-token prompt (~256 rows per expert: full two-m-tile
+    groups); trace bit-exact for every token, y checked on sampled tokens."""
+    c = inputs.CONFIGS["mixtral-8x7b"]
+    hm = harness.host_model(1, c["d"], c["ff"], c["n"], c["K"])
+    T = 1024
+    x, _ = harness.hidden_states(hm, T, "paper")
+    sample = [0, 1, 255, 256, 511, 700, 1022, 1023]
+    ref = _oracle_run(hm, x, N=1, M=c["n"], warm=True, tokens=sample)
+    y, tr, st = _prefill_run(hm, x, c["n"], True)
+    for f in EXACT_FIELDS:
+        np.testing.assert_array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    worst = max(float(np.abs(y[t, 0] - ref.y[t, 0]).max() / np.abs(ref.y[t, 0]).max()) for t in sample)
+    assert worst <= TOL, worst
+
+
 @pytest.mark.slow
 def test_prefill_mixtral_layer_256_tokens():
     c = inputs.CONFIGS["mixtral-8x7b"]
