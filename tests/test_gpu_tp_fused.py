@@ -166,3 +166,60 @@ def test_tp_without_nccl_or_connect_is_rejected():
         assert m.runtime_info()["tp_reduce"] == "none"
         e = m.tp_exchange_buffer()
         assert e["bytes"] == 256 + 2 * 2 * K * d * 8 and len(e["ipc_handle"]) == 64 and e["dev_ptr"]
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2512_16473_b200 import tp
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L, d, ff, n, K, T = 2, 256, 1024, 8, 2, 4
+        hp = harness.host_model(L, d, ff, n, K, tp_size=world, tp_rank=rank)
+        x, _ = harness.hidden_states(hp, T, "paper")
+        with harness.open_moe(hp, device=0) as m:
+            m.configure(ways=2, indexes=L)
+            how = tp.connect_peers(m)
+            y = harness.run_decode(m, x, device=0)
+            tr = m.trace()
+        q.put((rank, how, y, tr["expert"].copy(), tr["hit"].copy()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_reduce_two_processes_cuda_ipc():
+    """The multi-process wiring (one process per rank, as under torchrun): exchange buffers
+    mapped with CUDA IPC through tp.connect_peers (handles all-gathered over a gloo group),
+    both ranks on cuda:0 (their kernels time-slice the GPU). Same bar: bit-identical y on both
+    ranks, within 1e-4 of the unsplit oracle, routing equal to the oracle's."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=180) for _ in range(2)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    L, d, ff, n, K, T = 2, 256, 1024, 8, 2, 4
+    full = harness.host_model(L, d, ff, n, K)
+    x, _ = harness.hidden_states(full, T, "paper")
+    ref = oracle.decode(x, full.gates, lambda l, e: inputs.expert_weights(l, e, d, ff), N=L, M=2, K=K)
+    assert [r[1] for r in res] == ["fused-peer", "fused-peer"]
+    assert np.array_equal(res[0][2].view(np.uint32), res[1][2].view(np.uint32))
+    for r in res:
+        np.testing.assert_array_equal(r[3].astype(np.int64), ref.records["expert"].astype(np.int64))
+        np.testing.assert_array_equal(r[4].astype(np.int64), ref.records["hit"].astype(np.int64))
+    worst = max(float(np.abs(res[0][2][t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
+                for t in range(T) for l in range(L))
+    assert worst <= TIGHT, worst
