@@ -1,32 +1,38 @@
-// expert_fused.cu — K23: the whole expert FFN of one decode step in ONE persistent kernel
-// (sm_100a): SwiGLU gate/up GEMVs -> barrier -> down GEMV + gate-weighted combine.
+// expert_fused.cu — the whole decode step of one MoE layer in ONE kernel (sm_100a):
+// routing (gate GEMV, top-K, softmax, cache probe + LRU/FIFO/static update, miss handling),
+// then the SwiGLU expert GEMVs and the gate-weighted combine.
 //
+//   routing  z = Wg x; S = top-K(z); w = softmax(z_S); set l probed and updated
 //   phase A  h_r[j] = silu(W1_r[j,:] x) * (W3_r[j,:] x)              (R4)
 //   phase B  y[c]  += w_r * (W2_r[c,:] h_r)
 //
 // Decode batch 1 makes every expert matrix a GEMV (~1 FLOP/byte): an HBM stream, not a
-// tensor-core contraction. Design for B200:
-//  - one CTA per SM (grid = #SMs, cooperative => co-resident). Every CTA works on every
-//    expert, in the order A_o0, A_o1, B_o0, B_o1 (phase A = gate/up rows j, phase B = down
-//    rows c; resident experts before ones still being fetched): 88% of each segment's rows
-//    in static contiguous blocks, the tail claimed in small chunks from a per-segment
-//    counter (per-SM HBM bandwidth varies by ~10%; stealing evens it out over all SMs).
-//    h_r depends on every CTA's phase-A rows of expert r, but B_o0 only starts after
-//    A_o1 has been streamed, so the grid-wide dependency is resolved off the HBM critical
-//    path (per-stage release publications, acquire before the h copy). A CTA needs only
-//    ONE expert's h in shared memory at a time, which leaves room for a large weight ring;
+// tensor-core contraction. Design for B200 (DESIGN.md §6-§7):
+//  - one CTA per SM (grid = #SMs; co-residency checked at init), launched with programmatic
+//    dependent launch so the CTAs become resident while the previous call drains. Every CTA
+//    takes the routing decision itself from the same inputs (deterministic; CTA 0 alone
+//    writes the directory, trace, counters and miss mailbox): gate rows staged before the
+//    PDL wait, the GEMV spread over the consumer threads, a router warp publishing the slots
+//    through an mbarrier (all-hit fast path straight from the logits);
+//  - every CTA works on every routed expert, in the order A_o0, A_o1, B_o0, B_o1 (resident
+//    experts before ones still being fetched), rows scheduled static-then-steal (per-SM HBM
+//    bandwidth varies by ~10%; the stolen tail evens it out). h_r depends on every CTA's
+//    phase-A rows of expert r; B_o0 only starts after A_o1 has streamed, so the grid-wide
+//    dependency (per-stage release publications, acquire before the h copy) costs no HBM
+//    time;
 //  - warp 0 / lane 0 is a producer streaming weight rows with bulk async copies
 //    (cp.async.bulk — the TMA engine's linear path, SASS UBLKCP) into an NS-stage shared
-//    memory ring guarded by full/empty mbarriers (L2 evict-first). Bytes in flight per SM
-//    = the ring (~160 KB at Mixtral shapes), independent of how many consumer warps are
-//    still busy. W2 rows do not depend on h, so the producer streams through every
-//    phase and expert switch;
-//  - one consumer warp per ring stage: x (bf16) and then h_r (fp32, stored by phase A in
-//    a 2-plane layout and pulled in with ONE bulk copy) live in shared memory; fp32 FMAs,
-//    warp-shuffle reductions;
-//  - combine: y (zeroed by the router kernel) += w_r * o_r[c] with fire-and-forget fp32
-//    reductions. K <= 2 only: two addends onto 0 commute exactly, so y is bit-identical
-//    to the oracle's rank-ordered sum; other K take the split path.
+//    memory ring guarded by full/empty mbarriers (L2 evict-first): phase A one W1+W3 row pair
+//    per stage, phase B RB whole W2 rows per pair of stages. W2 rows do not depend on h, so
+//    the producer streams through every phase and expert switch;
+//  - consumers: 2 warps per phase-A stage (x as bf16, mixed-precision FMAs), 4 per phase-B
+//    pair (h_r as fp32 in a 2-plane layout), fixed-order combination of the partials;
+//  - merged phase B (small ff_r: every expert's h fits beside x): the router warp copies each
+//    h_r in as soon as it is published and B_o0 / B_o1 stream without a switch;
+//  - combine: y (zeroed by every CTA for its slice) += w_r * o_r[c] with fire-and-forget
+//    fp32 reductions — K <= 2: two addends onto 0 commute, so y is bit-reproducible; other K
+//    take the split path. Tensor parallel (f3): every term goes to every rank as a tagged
+//    8-byte word instead, summed in a fixed order in the epilogue.
 #include <math.h>
 
 #include "moe_internal.cuh"
@@ -184,8 +190,9 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
 constexpr int kChunkA = 2;     // phase A rows per tail claim
 constexpr int kChunkB = 1;     // phase B rows per tail claim
 
-// Ring-slot meta word: >= 0 a weight row (phase A: (r << 24) | j, phase B: c);
-// kEnd closes a phase; kSegB switches phase B to the next expert; kSegA - r closes
+// Ring-slot meta word: >= 0 a weight chunk (phase A: (r << 24) | j, the W1/W3 row pair j
+// of expert r; phase B: (r << 24) | c, W2 rows c .. c + metaN - 1); kEnd closes a phase;
+// kSegB switches phase B to the next expert (segmented phase B only); kSegA - r closes
 // phase-A segment r in this stage (its h writer publishes the rows it wrote).
 constexpr int kEnd = -1;
 constexpr int kSegB = -2;
