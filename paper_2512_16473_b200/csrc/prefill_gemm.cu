@@ -19,7 +19,10 @@ namespace {
 
 using namespace tc;
 
-constexpr int kThreadsTC = 192;
+// warps 0-3 and 6-9: epilogue (TMEM lane quarter = warp % 4, column half = warp >= 6);
+// warp 4: TMA producer; warp 5: MMA issuer
+constexpr int kThreadsTC = 320;
+constexpr int kEpiWarps = 8;
 
 // MT m-tiles per CTA tile share every B (weight) tile: operand bytes per FLOP drop by
 // (1 + NB*BN/BM) / (MT + NB*BN/BM) — the GEMMs are bound by the TMA / L2 -> SM stream
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(tfull + a, 1);
-      ptx::mbar_init(tempty + a, 4);   // one arrival per epilogue warp
+      ptx::mbar_init(tempty + a, kEpiWarps);   // one arrival per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -208,7 +211,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 0-3)
-    const int row = warp * 32 + lane;                      // accumulator row = TMEM lane
+    const int quarter = warp & 3, chalf = warp >= 6 ? 1 : 0;
+    const int row = quarter * 32 + lane;                   // accumulator row = TMEM lane
+    const int cb = chalf * (BN / 2), ce = cb + BN / 2;      // this warp's half of the columns
     int tl = 0;
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++tl) {
       const TileCoord tc = tile_of<MT>(p, BN, id);
@@ -216,10 +221,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
       ptx::mbar_wait(tfull + acc, (tl / kBufs) & 1);
       tc_fence_after();
       for (int i = 0; i < tc.nm; ++i) {
-        const uint32_t tbase = tmem + acc * kAcc + i * NB * BN + ((uint32_t)(warp * 32) << 16);
+        const uint32_t tbase = tmem + acc * kAcc + i * NB * BN + ((uint32_t)(quarter * 32) << 16);
         const int orow = tc.out_row + i * BM + row;
         if (p.mode == TC_MODE_PLAIN) {
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = cb; c < ce; c += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + c, v);
             if (orow < p.M) {
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
           }
         } else if (p.mode == TC_MODE_SWIGLU) {
           // h = silu(g) * u  (R4), rounded to bf16 for the second GEMM's A operand
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = cb; c < ce; c += 32) {
             uint32_t g[32], u[32];
             tmem_ld32(tbase + c, g);
             tmem_ld32(tbase + BN + c, u);
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
           // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
           const int tok = p.plan->tok[orow];
           const float w = p.plan->wrow[orow];
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = cb; c < ce; c += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + c, v);
             if (tok >= 0 && tc.out_col + c < p.N) {
