@@ -853,9 +853,13 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;
-  p->pctA = 88;
-  p->pctB = 40;
   p->RB = min(kMaxRB, (2 * SB) / (2 * ffr));     // W2 rows per phase-B super-stage
+  // static shares (rest stolen in chunks): measured on B200 across the BASELINE shapes
+  // (bench_shapes.py sweeps): 95% of phase A; 10% of phase B with 1-2-row chunks, 20% with
+  // bigger ones (8x22B slices) — phase B's expert switch and the end of the step leave the
+  // CTAs unevenly advanced, and a long stolen tail re-balances them
+  p->pctA = 95;
+  p->pctB = p->RB <= 2 ? 10 : 20;
   p->merge = merge ? 1 : 0;
   p->hoff = hoff;
   p->hstride = hstride;
