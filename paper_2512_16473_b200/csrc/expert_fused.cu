@@ -190,13 +190,13 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
 constexpr int kChunkA = 2;     // phase A rows per tail claim
 constexpr int kChunkB = 1;     // phase B rows per tail claim
 
-// Ring-slot meta word: >= 0 a weight chunk (phase A: (r << 24) | j, the W1/W3 row pair j
-// of expert r; phase B: (r << 24) | c, W2 rows c .. c + metaN - 1); kEnd closes a phase;
-// kSegB switches phase B to the next expert (segmented phase B only); kSegA - r closes
-// phase-A segment r in this stage (its h writer publishes the rows it wrote).
+// Ring-slot meta word: >= 0 a weight chunk (phase A: (si << 24) | j, the W1/W3 row pair j
+// of segment si's expert; phase B: (r << 24) | c, W2 rows c .. c + metaN - 1 of expert r);
+// kEnd closes a phase; kSegB switches phase B to the next expert (segmented phase B only).
+// Phase A has no segment markers: a stage's h writer publishes its rows of a segment when
+// it meets the next segment's first row, or at kEnd.
 constexpr int kEnd = -1;
 constexpr int kSegB = -2;
-constexpr int kSegA = -3;
 
 // Static-then-steal schedule over `total` rows for CTA b of G: the first pct% of
 // the rows are split into equal contiguous blocks, the tail is claimed in chunks from a
@@ -229,8 +229,8 @@ __device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct)
 //
 // Work order (all CTAs, no group split): phase A of every device-computed expert in turn
 // (A_o0, A_o1), then phase B (B_o0, B_o1). h_r is complete once every stage of every CTA
-// has passed the kSegA marker that closes A_r; each stage's single h writer publishes its
-// own rows then (release RED on bar[r]). B_o0 starts only after A_o1 has streamed, so its
+// has moved past segment A_r (the next segment's first row, or kEnd); each stage's single
+// h writer publishes its own rows then (release RED on bar[r]). B_o0 starts only after A_o1 has streamed, so its
 // wait on bar[o0] is normally already satisfied: the grid-wide dependency costs no HBM time.
 __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedArgs f) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           acquire(s);
           const uint8_t* w1 = base + (long long)j * d * 2;
           const uint8_t* w3 = w1 + (long long)ffr * d * 2;
-          meta[s] = (r << 24) | j;
+          meta[s] = (si << 24) | j;
           mbar_arrive_expect_tx(full + s, (uint32_t)rowA);
           bulk_g2s(ring + (size_t)s * SB, w1, 2u * d, full + s, pol);
           bulk_g2s(ring + (size_t)s * SB + 2 * d, w3, 2u * d, full + s, pol);
@@ -521,7 +521,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           if (sa.tail0 + (int)c1 < ffr) c2 = atomicAdd(cA, (unsigned)kChunkA);
           for (int j = j0; j < j1; ++j) issue_a(j);
         }
-        marker_a(kSegA - r);  // every stage publishes its rows of h_r
+        // no marker between segments: a stage's consumers see the segment index change in
+        // the row meta (its h writer then publishes the rows it wrote of the earlier
+        // segment), so the ring does not drain at the expert switch
       }
       if (f.ts) f.ts[b * kTsPerCta + 12] = globaltimer();  // last phase-A row issued
       marker_a(kEnd);
@@ -627,22 +629,19 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const int4* w1 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB);
     const int4* w3 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB + 2 * d);
     bool first = true;
+    int pubseg = 0;                        // (h writer) first segment not yet published
     while (true) {
       mbar_wait(full + sA, ph);
       ph ^= 1;
       const int m = meta[sA];
-      if (m < 0) {
-        if (m == kEnd) break;
-        // end of segment r in this stage: its h writer (half 0, lane 0) wrote every row of
-        // h_r this stage produced; publish them (release at gpu scope covers its own stores)
-        named_bar_sync(2 + sA, 64);        // both halves read meta before the stage is reused
-        if (half == 0 && lane == 0) {
-          mbar_arrive(empty + sA);
-          red_release_add_u64(f.bar + 16 * (kSegA - m), 1ull);
-        }
-        continue;
-      }
-      const int r = m >> 24, j = m & 0xFFFFFF;
+      if (m < 0) break;                    // kEnd
+      const int si = m >> 24, j = m & 0xFFFFFF;
+      const int r = sorder[si];
+      // a row of a later segment: this stage's h writer (half 0, lane 0) has written every
+      // row of the earlier segments it produced; publish them (release at gpu scope covers
+      // its own stores)
+      if (half == 0 && lane == 0)
+        for (; pubseg < si; ++pubseg) red_release_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
       if (f.ts && first && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 2] = globaltimer();
       first = false;
       float2 g = make_float2(0.f, 0.f), u = make_float2(0.f, 0.f);
@@ -666,6 +665,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         a.h[(long long)r * ffr + h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
       }
     }
+    if (half == 0 && lane == 0)            // the rest of this stage's segments
+      for (const int nseg = snseg; pubseg < nseg; ++pubseg) red_release_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
     named_bar_sync(2 + sA, 64);
     if (half == 0 && lane == 0) mbar_arrive(empty + sA);  // release the end marker's stage
     if (half == 0 && lane == 0 && (sA & 1) == 0) {
