@@ -176,9 +176,11 @@ MOE_API moe_status moe_layer_forward(moe_ctx* ctx, int32_t layer, const void* x,
  * K <= 2, d % 64 == 0, (ff/P) % 128 == 0. First-touch misses are fetched into their slots. */
 MOE_API moe_status moe_layer_prefill(moe_ctx* ctx, int32_t layer, const void* x, float* y, int32_t T, void* stream);
 
-/* End-to-end variant of moe_layer_forward with HOST buffers: copies x (bf16 [d], best
- * pinned) host->device, runs the layer on the context's own stream, copies y (fp32 [d])
- * device->host and synchronizes. */
+/* End-to-end variant of moe_layer_forward with HOST buffers x (bf16 [d]) and y (fp32 [d]):
+ * runs the layer on the context's own stream and synchronizes (polling). With pinned,
+ * device-mapped buffers (cudaHostAlloc / moe_host_alloc / torch pin_memory, 16-B aligned) on
+ * the fused path the kernel reads x from and writes y to host memory itself (zero-copy);
+ * otherwise x and y are copied with cudaMemcpyAsync around the kernel. */
 MOE_API moe_status moe_layer_forward_host(moe_ctx* ctx, int32_t layer, const uint16_t* x_host, float* y_host);
 
 /* Per-layer counters (Fig.6 hit-rate definitions; SPEC CacheStats S:203-207).

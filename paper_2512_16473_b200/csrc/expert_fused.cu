@@ -142,7 +142,7 @@ __device__ __forceinline__ void tp_push(const FusedArgs& f, int r, int c, float 
   for (int p = 0; p < f.tpP; ++p) st_relaxed_sys_u64(tp_slot(f, p, f.tp_rank, r, c), w);
 }
 __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, int G, int ctid, int nthr) {
-  const int P = f.tpP, K = f.e.K, d = f.e.d, PK = P * K;  // PK in {2, 4, 8, 16}: divides 32 and nthr
+  const int P = f.tpP, K = f.e.K, d = f.e.d, PK = P * K;  // PK in {1, 2, 4, 8, 16}: divides 32 and nthr
   const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
   const int total = (c1 - c0) * PK;
   const unsigned long long tag = tp_tag(f);
@@ -313,7 +313,28 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 8] = globaltimer();
   DirState ds;
   if (warp == kRouterWarp) ds = dir_load(ra, lane);  // the router's directory loads in flight
+  if (f.xhost && b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + nthr) {
+    // moe_layer_forward_host: x is read straight from the caller's pinned host buffer (one
+    // PCIe pass, by CTA 0) into the device staging buffer a.x, then published to every CTA
+    // (no copy-engine transfer queued in front of the kernel)
+    const int i = threadIdx.x - 32;
+    for (int k = i; k < (d >> 3); k += nthr)
+      reinterpret_cast<int4*>(const_cast<uint16_t*>(a.x))[k] = reinterpret_cast<const int4*>(f.xhost)[k];
+    named_bar_sync(12, nthr);
+    if (i == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.xflag), "r"(f.xseq) : "memory");
+    }
+  }
   if (threadIdx.x == 0) {
+    if (f.xhost) {                            // wait for CTA 0's copy of x
+      const unsigned long long t0 = globaltimer();
+      while ((int)(ld_acquire_u32(f.xflag) - f.xseq) < 0) {
+        __nanosleep(32);
+        if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     mbar_arrive_expect_tx(&xbar, 2u * d);
     bulk_g2s(xh, a.x, 2u * d, &xbar, policy_evict_last());
   }
@@ -766,7 +787,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + s);  // (partials read first: the next rows rewrite them)
           if (lane < nr) {
-            if (f.tpP > 1) tp_push(f, r, c + lane, w * o);  // f3: straight to every rank
+            if (f.tpP > 0) tp_push(f, r, c + lane, w * o);  // f3 / LL: straight to every rank
             else if (K == 1) a.y[c + lane] = w * o;
             else red_add_f32(a.y + c + lane, w * o);  // K == 2: 0 + a + b is order-independent
           }
@@ -797,12 +818,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const float* o = a.host_out + (size_t)r * d;
     for (int c = c0 + ctid; c < c1; c += nthr) {
       const float v = w * __ldcg(o + c);
-      if (f.tpP > 1) tp_push(f, r, c, v);
+      if (f.tpP > 0) tp_push(f, r, c, v);
       else if (K == 1) a.y[c] = v;
       else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
     }
   }
-  if (f.tpP > 1) tp_reduce_epilogue(f, b, G, ctid, nthr);
+  if (f.tpP > 0) tp_reduce_epilogue(f, b, G, ctid, nthr);
   if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 5] = globaltimer();
   if (f.sts && cw == 0 && lane == 0) f.sts[kStsHead + G + b] = globaltimer();
 }

@@ -112,6 +112,12 @@ struct FusedArgs {
   unsigned long long tp_calls;    // earlier fused-TP calls on this context (same on every rank)
   uint8_t* peer[8];               // exchange buffer base of every rank (peer[tp_rank] = own)
   float* yout;                    // [d] all-reduced y (caller's buffer)
+  // moe_layer_forward_host: x is read from this (device-accessible) pinned host pointer by
+  // CTA 0 into e.x, which then releases xseq on *xflag; every CTA acquires it before loading
+  // x. nullptr: x is ready in e.x.
+  const uint16_t* xhost;
+  uint32_t* xflag;
+  uint32_t xseq;
 };
 // Exchange buffer of one TP rank: slots[2][d][P][K] u64 at kTpSlotOff (call parity, column,
 // source rank, routing rank), each word {fp32 term w_r * o_r[c] | call tag << 32}, written

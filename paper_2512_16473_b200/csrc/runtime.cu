@@ -156,6 +156,10 @@ struct moe_ctx {
   // end-to-end buffers
   uint16_t* d_x_e2e = nullptr;
   float* d_y_e2e = nullptr;
+  uint32_t* d_xflag = nullptr;       // x staged by CTA 0 from host memory (zero-copy forward_host)
+  uint32_t xseq = 0;
+  uint8_t* d_ll1 = nullptr;          // single-rank LL slots: y written straight to host memory
+  unsigned long long ll_calls = 0;
   // profiling
   bool prof = false;
   std::vector<ProfEv> prof_events;
@@ -530,6 +534,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMalloc(&c->d_h, sizeof(float) * (size_t)K * c->ffr));
   INIT_TRY(cudaMalloc(&c->d_x_e2e, sizeof(uint16_t) * d));
   INIT_TRY(cudaMalloc(&c->d_y_e2e, sizeof(float) * d));
+  INIT_TRY(cudaMalloc(&c->d_xflag, sizeof(uint32_t)));
+  INIT_TRY(cudaMemset(c->d_xflag, 0, sizeof(uint32_t)));
   INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * 2 * kMaxK));
@@ -628,6 +634,8 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_h);
   cudaFree(c->d_x_e2e);
   cudaFree(c->d_y_e2e);
+  cudaFree(c->d_xflag);
+  cudaFree(c->d_ll1);
   cudaFree(c->d_bar);
   cudaFree(c->d_ctr);
   cudaFree(c->d_hout);
@@ -789,13 +797,17 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   return MOE_OK;
 }
 
-static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* y, cudaStream_t s) {
+// xhost / yhost (moe_layer_forward_host, fused path): device-accessible pinned host buffers;
+// the kernel reads x from xhost into the staging buffer x and writes y straight to yhost.
+static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* y, cudaStream_t s,
+                               const uint16_t* xhost = nullptr, float* yhost = nullptr) {
   if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
   if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
   if (!x || !y) return fail(MOE_ERR_INVALID_ARG, "NULL x or y");
   if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(MOE_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
   if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
   const bool tpf = c->P > 1 && c->tp_fused && c->fused;  // y summed in the kernel's epilogue (f3)
+  const bool ll1 = yhost && !tpf && c->fused;             // single-rank LL: y -> host memory
   if (c->P > 1 && !tpf && !c->comm)
     return fail(MOE_ERR_STATE, "tp_size > 1 without an NCCL communicator needs moe_tp_connect_* (fused path)");
   // host-side back-pressure: never let the GPU overwrite an unconsumed mailbox entry
@@ -834,7 +846,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ea.x = (const uint16_t*)x;
   ea.d = c->d; ea.ffr = c->ffr; ea.K = c->K;
   ea.h = c->d_h;
-  ea.y = tpf ? c->d_ypart : y;
+  ea.y = (tpf || ll1) ? c->d_ypart : y;
   ea.ready = c->d_ready;
   ea.last_seq = c->d_last;
   ea.seq = seq;
@@ -863,11 +875,15 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
     fa.sts = ra.sts;
-    fa.tpP = tpf ? c->P : 0;
-    fa.tp_rank = c->rank;
-    fa.tp_calls = c->tp_calls;
+    fa.tpP = tpf ? c->P : ll1 ? 1 : 0;
+    fa.tp_rank = tpf ? c->rank : 0;
+    fa.tp_calls = tpf ? c->tp_calls : c->ll_calls;
     for (int p = 0; p < 8; ++p) fa.peer[p] = tpf && p < c->P ? c->tp_peer[p] : nullptr;
-    fa.yout = y;
+    if (ll1) fa.peer[0] = c->d_ll1;
+    fa.yout = yhost ? yhost : y;
+    fa.xhost = xhost;
+    fa.xflag = c->d_xflag;
+    fa.xseq = xhost ? ++c->xseq : 0u;
     prof_begin(c, 1, s, &pe);
     cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl, c->coop);
     if (e != cudaSuccess && c->pdl) {  // PDL not accepted: retry without it
@@ -879,6 +895,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("expert_fused launch: ") + cudaGetErrorString(e));
     c->fused_calls += 1;
     if (tpf) c->tp_calls += 1;
+    if (ll1) c->ll_calls += 1;
     c->issued.store(seq, std::memory_order_release);  // the fetch thread may now wait for it
   } else {
     prof_begin(c, 0, s, &pe);
@@ -1036,10 +1053,32 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint1
   if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
   DeviceGuard g(c->device);
   cudaStream_t s = c->own_stream;
-  CUDA_TRY(cudaMemcpyAsync(c->d_x_e2e, x_host, sizeof(uint16_t) * c->d, cudaMemcpyHostToDevice, s));
-  moe_status st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s);
-  if (st != MOE_OK) return st;
-  CUDA_TRY(cudaMemcpyAsync(y_host, c->d_y_e2e, sizeof(float) * c->d, cudaMemcpyDeviceToHost, s));
+  moe_status st;
+  // Zero-copy (fused path, pinned host buffers): the kernel reads x from the host buffer and
+  // writes y straight into it — no copy-engine transfer queued in front of or behind it.
+  void* xd = nullptr;
+  void* yd = nullptr;
+  const bool zc = c->fused && (c->P == 1 || c->tp_fused) &&
+                  cudaHostGetDevicePointer(&xd, (void*)x_host, 0) == cudaSuccess &&
+                  cudaHostGetDevicePointer(&yd, (void*)y_host, 0) == cudaSuccess && c->d % 8 == 0 &&
+                  ((uintptr_t)xd & 15) == 0 && ((uintptr_t)yd & 15) == 0;
+  cudaGetLastError();
+  if (zc && !c->tp_fused && !c->d_ll1) {
+    const long long bytes = tp_xchg_bytes(1, c->K, c->d);
+    CUDA_TRY(cudaMalloc(&c->d_ll1, (size_t)bytes));
+    CUDA_TRY(cudaMemset(c->d_ll1, 0, (size_t)bytes));
+    if (!c->d_ypart) CUDA_TRY(cudaMalloc(&c->d_ypart, sizeof(float) * c->d));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
+  if (zc) {
+    st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s, (const uint16_t*)xd, (float*)yd);
+    if (st != MOE_OK) return st;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(c->d_x_e2e, x_host, sizeof(uint16_t) * c->d, cudaMemcpyHostToDevice, s));
+    st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s);
+    if (st != MOE_OK) return st;
+    CUDA_TRY(cudaMemcpyAsync(y_host, c->d_y_e2e, sizeof(float) * c->d, cudaMemcpyDeviceToHost, s));
+  }
   // Latency-oriented wait (single-request decode): poll the completion event instead of a
   // blocking synchronize, whose OS wake-up costs ~10 us per call.
   CUDA_TRY(cudaEventRecord(c->host_ev, s));

@@ -178,6 +178,34 @@ def test_host_entry_point_matches(tiny):
         _compare(tiny, m, x, ref, y)
 
 
+@pytest.mark.parametrize("mode", [moe.MISS_FETCH, moe.MISS_HOST_COMPUTE])
+def test_host_entry_point_zero_copy_pinned(tiny, mode):
+    """moe_layer_forward_host with PINNED host buffers takes the zero-copy path (CTA 0 reads x
+    from host memory, y is written to host memory by the single-rank LL epilogue) — same bits
+    as the device entry point."""
+    x, _ = harness.hidden_states(tiny, 8, "paper")
+    ref = _oracle_run(tiny, x, N=3, M=2)
+    xb = moe.PinnedBuffer(tiny.d * 2)
+    yb = moe.PinnedBuffer(tiny.d * 4)
+    xv, yv = xb.array.view(np.uint16), yb.array.view(np.float32)
+    with harness.open_moe(tiny) as m:
+        m.configure(ways=2, indexes=3, miss_mode=mode)
+        y = np.zeros((8, tiny.L, tiny.d), np.float32)
+        for t in range(8):
+            for l in range(tiny.L):
+                xv[:] = x[t, l]
+                yv[:] = np.nan
+                m.forward_host(l, xv, yv)
+                y[t, l] = yv
+        _compare(tiny, m, x, ref, y)
+    with harness.open_moe(tiny) as m:  # the device entry point on the same calls: identical bits
+        m.configure(ways=2, indexes=3, miss_mode=mode)
+        yd = harness.run_decode(m, x)
+    assert np.array_equal(y.view(np.uint32), yd.view(np.uint32))
+    xb.free()
+    yb.free()
+
+
 def test_delayed_fetch_hit_under_fill_is_waited_on():
     """Fault injection: the fetch thread sleeps 3 ms before each copy, so the expert
     kernels must wait on the slots' ready generations; a kernel that read a slot before
