@@ -22,3 +22,18 @@ with harness.open_moe(hm) as m:
 ok = all(np.array_equal(tr[f].astype(int), ref.records[f].astype(int)) for f in ("expert", "hit", "way", "evicted"))
 err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()) for t in range(6) for l in range(4))
 print("warm all-hit bitexact", ok, "err", err, flush=True)
+# zero-copy host entry point (pinned buffers): CTA 0 reads x from host memory, y written to host memory
+xb, yb = moe.PinnedBuffer(hm.d * 2), moe.PinnedBuffer(hm.d * 4)
+xv, yv = xb.array.view(np.uint16), yb.array.view(np.float32)
+ref = oracle.decode(x, hm.gates, lambda l, e: inputs.expert_weights(l, e, hm.d, hm.ff), N=3, M=2, K=2)
+with harness.open_moe(hm) as m:
+    m.configure(ways=2, indexes=3)
+    worst = 0.0
+    for t in range(6):
+        for l in range(4):
+            xv[:] = x[t, l]
+            m.forward_host(l, xv, yv)
+            worst = max(worst, float(np.abs(yv - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()))
+    tr = m.trace()
+ok = all(np.array_equal(tr[f].astype(int), ref.records[f].astype(int)) for f in ("expert", "hit", "way", "evicted"))
+print("zero-copy host entry bitexact", ok, "err", worst, flush=True)
