@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // Gate GEMV z = Wg x: a few KFLOP, latency-bound — spread over every consumer
     // thread instead of a dependent chain of MMAs: thread i takes 16-B chunks i, i + nthr, ...
     // of x and of 8 gate rows at a time (sm_100 mixed-precision FMAs, bf16 products exact
-    // in fp32), then a warp-shuffle tree per expert. Per-warp partials, reduced in a fixed
+    // in fp32), then a warp reduce-scatter over the 8 experts. Per-warp partials, reduced in a fixed
     // order by the router warp (deterministic).
     mbar_wait(&gbar, 0);
     if (pm && threadIdx.x == 32) pm[0] = clock64();
@@ -371,11 +371,24 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
             if (e0 + j < n)
               acc[j] = dot8_bf(reinterpret_cast<const int4*>(ring + (size_t)(e0 + j) * gstride)[ch], xv, acc[j]);
         }
+        // reduce-scatter over the warp (9 shuffles instead of 8 x 5): after the xor-16/8/4
+        // steps lane L holds expert 4*L[4] + 2*L[3] + L[2] summed over 8 lanes, then xor-2/1
+        float v[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float z = warp_sum(acc[j].x + acc[j].y);
-          if (lane == 0 && e0 + j < n) zpart[cw * n + e0 + j] = z;
-        }
+        for (int j = 0; j < 8; ++j) v[j] = acc[j].x + acc[j].y;
+        const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+        float w4[4], w2[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)  // keep half b4 of the 8, send the other half
+          w4[i] = (b4 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, b4 ? v[i] : v[i + 4], 16);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          w2[i] = (b3 ? w4[i + 2] : w4[i]) + __shfl_xor_sync(0xffffffffu, b3 ? w4[i] : w4[i + 2], 8);
+        float z = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
+        z += __shfl_xor_sync(0xffffffffu, z, 2);
+        z += __shfl_xor_sync(0xffffffffu, z, 1);
+        const int e = e0 + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+        if ((lane & 3) == 0 && e < n) zpart[cw * n + e] = z;
       }
     }
     if (pm && threadIdx.x == 32) pm[2] = clock64();
