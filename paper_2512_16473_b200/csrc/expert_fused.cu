@@ -560,6 +560,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         // segment), so the ring does not drain at the expert switch
       }
       if (f.ts) f.ts[b * kTsPerCta + 12] = globaltimer();  // last phase-A row issued
+      if (f.prefetchB && nseg > 0 && !swait[sorder[0]]) {
+        // the ring drains before phase B starts: have this CTA's first W2 rows on their way
+        // to L2 meanwhile (same bytes, read from HBM once)
+        const RowSched sb0 = make_sched(d, b, G, f.pctB);
+        const int nr = min(NSB * RB, sb0.s1 - sb0.s0);
+        if (nr > 0) bulk_prefetch_l2(sbase[sorder[0]] + w2off + (long long)sb0.s0 * rowB, (uint32_t)(nr * rowB));
+      }
       marker_a(kEnd);
       // phase B: whole W2 rows into super-stages (2u, 2u+1); W2 does not depend on h, so
       // these loads stream while the consumers finish phase A and load h
@@ -896,6 +903,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->pctA = 95;
   p->pctB = p->RB <= 2 ? 10 : 20;
   p->merge = merge ? 1 : 0;
+  p->prefetchB = 1;
   p->hoff = hoff;
   p->hstride = hstride;
   p->smem = (size_t)NS * SB + xh + tail;

@@ -102,6 +102,7 @@ struct FusedArgs {
   int pctA, pctB;                 // share of phase A / B rows assigned statically (rest: stolen)
   int RB;                         // W2 rows per phase-B super-stage
   int merge;                      // 1: merged phase B when every routed expert is resident and ready
+  int prefetchB;                  // 1: L2 prefetch of the first W2 rows at the end of phase A
   int hoff, hstride;              // merged: h_r at xh + hoff + r * hstride
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
@@ -125,7 +126,7 @@ struct FusedArgs {
 constexpr int kTpSlotOff = 256;
 inline long long tp_xchg_bytes(int P, int K, int d) { return kTpSlotOff + 2ll * P * K * d * 8; }
 struct FusedPlan {
-  int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, hoff, hstride;
+  int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, prefetchB, hoff, hstride;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

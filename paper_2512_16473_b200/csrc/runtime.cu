@@ -565,6 +565,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       const char* pb = getenv("MOE_STATIC_B");
       if (pa && atoi(pa) >= 0 && atoi(pa) <= 100) c->plan.pctA = atoi(pa);
       if (pb && atoi(pb) >= 0 && atoi(pb) <= 100) c->plan.pctB = atoi(pb);
+      const char* pfb = getenv("MOE_PREFETCH_B");  // L2 prefetch of the first W2 rows (default on)
+      if (pfb && pfb[0] == '0') c->plan.prefetchB = 0;
       const char* mg = getenv("MOE_MERGE");   // merged phases (default: when the plan allows)
       if (mg && mg[0] == '0') c->plan.merge = 0;
       const char* rb = getenv("MOE_ROWS_B");  // W2 rows per phase-B super-stage (<= plan's)
@@ -870,6 +872,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.pctB = c->plan.pctB;
     fa.RB = c->plan.RB;
     fa.merge = c->plan.merge;
+    fa.prefetchB = c->plan.prefetchB;
     fa.hoff = c->plan.hoff;
     fa.hstride = c->plan.hstride;
     fa.dbg = c->d_dbg;
