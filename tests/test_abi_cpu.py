@@ -35,6 +35,8 @@ def test_struct_layouts_match_header():
     assert _abi.RECORD_DTYPE.itemsize == 20
     assert ctypes.sizeof(_abi.CacheConfig) == 56
     assert ctypes.sizeof(_abi.ModelDesc) == 40
+    assert ctypes.sizeof(_abi.RuntimeInfo) == 32
+    assert ctypes.sizeof(_abi.TpExchange) == 80   # {void*, int64, uint8[64]}
 
 
 @pytest.mark.parametrize("shape,msg", [((0, 64, 128, 8, 2), "bad shape"), ((4, 60, 128, 8, 2), "bad shape"),
@@ -84,3 +86,15 @@ def test_host_expert_ffn_matches_oracle(d, ff):
         out = moe.host_expert_ffn(blob, x, d, ff, threads=thr)
         assert np.abs(out - ref).max() <= 1e-5 * np.abs(ref).max()
     assert np.array_equal(moe.host_expert_ffn(blob, x, d, ff, 1), moe.host_expert_ffn(blob, x, d, ff, 4))
+
+
+def test_tp_connect_validation_without_gpu():
+    """moe_tp_connect_local rejects bad arguments before touching any context."""
+    lib = moe.lib()
+    assert lib.moe_tp_connect_local(None, 2) == 1
+    arr = (ctypes.c_void_p * 1)(None)
+    assert lib.moe_tp_connect_local(arr, 1) == 1      # P < 2
+    assert lib.moe_tp_connect_local(arr, 9) == 1      # P > 8
+    assert lib.moe_tp_connect_ipc(None, None) == 1
+    assert lib.moe_tp_exchange_buffer(None, None) == 1
+    assert lib.moe_tp_disconnect(None) == 1
