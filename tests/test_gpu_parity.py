@@ -492,11 +492,13 @@ def test_fused_path_odd_shapes(L, d, ff, n, K, M, T):
 
 @pytest.mark.parametrize("env", [{"MOE_EXPERT_PATH": "split"}, {"MOE_COOP": "1"}, {"MOE_PDL": "0"},
                                  {"MOE_STATIC_A": "0", "MOE_STATIC_B": "0"},
-                                 {"MOE_STATIC_A": "100", "MOE_STATIC_B": "100"}])
+                                 {"MOE_STATIC_A": "100", "MOE_STATIC_B": "100"},
+                                 {"MOE_MERGE": "0"}, {"MOE_PREFETCH_B": "0"}, {"MOE_ROWS_B": "1"}])
 def test_launch_and_schedule_variants(tiny, monkeypatch, env):
     """Every launch / schedule variant the runtime can take gives the same bit-exact trace and
     outputs: the split fallback, the cooperative launch, no PDL, all-stolen and all-static
-    row schedules (the work-claim counters at their extremes)."""
+    row schedules (the work-claim counters at their extremes), the segmented phase B where
+    the merged one would run, no W2 prefetch, one W2 row per phase-B chunk."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     x, ranked = harness.hidden_states(tiny, 24, "paper")
@@ -507,3 +509,10 @@ def test_launch_and_schedule_variants(tiny, monkeypatch, env):
         m.configure(ways=2, indexes=3)
         y = harness.run_decode(m, x)
         _compare(tiny, m, x, ref, y)
+    if "MOE_EXPERT_PATH" not in env:   # the fused variants also agree bit for bit with the default
+        for k in env:
+            monkeypatch.delenv(k)
+        with harness.open_moe(tiny) as m:
+            m.configure(ways=2, indexes=3)
+            y0 = harness.run_decode(m, x)
+        assert np.array_equal(y.view(np.uint32), y0.view(np.uint32))
