@@ -41,6 +41,8 @@ def main():
                     help="fetch: fill the victim slot then compute on the GPU (B200 design); "
                          "host: host cores compute the miss while it is post-fetched (paper P:199-201)")
     ap.add_argument("--host-threads", type=int, default=0)
+    ap.add_argument("--warm", action="store_true",
+                    help="warm start: experts 0..M-1 of every layer preloaded (M = n: every access hits)")
     args = ap.parse_args()
     import torch
 
@@ -72,11 +74,12 @@ def main():
     t_oracle = time.time() - t1
     out = []
     for M in [int(v) for v in args.ways.split(",")]:
-        ref = oracle.decode(x, hm.gates, None, N=L, M=M, K=c["K"], compute=False)   # routing + cache replay
+        ref = oracle.decode(x, hm.gates, None, N=L, M=M, K=c["K"], compute=False,   # routing + cache replay
+                            warm_start=args.warm)
         with harness.open_moe(hm) as m:
             import paper_2512_16473_b200 as moe
             mm = moe.MISS_HOST_COMPUTE if args.miss_mode == "host" else moe.MISS_FETCH
-            geo = m.configure(ways=M, indexes=L, miss_mode=mm, host_threads=args.host_threads)
+            geo = m.configure(ways=M, indexes=L, miss_mode=mm, host_threads=args.host_threads, warm_start=args.warm)
             s = torch.cuda.Stream(dev)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             for t in range(T):
@@ -99,6 +102,7 @@ def main():
         timed_fetch = int((rec["hit"] == 0).sum())
         line = {
             "config": args.config, "miss_mode": args.miss_mode, "layers": L, "ways": M, "indexes": L,
+            "start": "warm" if args.warm else "cold",
             "geometry": geo,
             "tokens_timed": T - 1, "ms": ms, "tokens_per_s": (T - 1) / (ms * 1e-3),
             "ms_per_layer": ms / ((T - 1) * L),
