@@ -475,6 +475,26 @@ def test_prefill_mixtral_layer_256_tokens():
     assert worst <= TOL, worst
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name,warm,T", [("phi-3.5-moe", False, 512), ("mixtral-8x22b", True, 384)])
+def test_prefill_other_baseline_shapes_sampled(name, warm, T):
+    """f4 at the other BASELINE expert shapes: Phi-3.5-MoE (n = 16, ff = 6400, cold start, so
+    each expert's first access in the prompt is a fetched miss) and one unsplit Mixtral-8x22B
+    layer (d = 6144, ff = 16384). Trace and counters bit-exact for every token, y on samples."""
+    c = inputs.CONFIGS[name]
+    hm = harness.host_model(1, c["d"], c["ff"], c["n"], c["K"])
+    x, _ = harness.hidden_states(hm, T, "paper")
+    sample = [0, 1, 127, 128, T // 2, T - 2, T - 1]
+    ref = _oracle_run(hm, x, N=1, M=c["n"], warm=warm, tokens=sample)
+    y, tr, st = _prefill_run(hm, x, c["n"], warm)
+    for f in EXACT_FIELDS:
+        np.testing.assert_array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    for k in STAT_KEYS:
+        assert st[0][k] == ref.stats[0][k], k
+    worst = max(float(np.abs(y[t, 0] - ref.y[t, 0]).max() / np.abs(ref.y[t, 0]).max()) for t in sample)
+    assert worst <= TOL, worst
+
+
 @pytest.mark.parametrize("L,d,ff,n,K,M,T", [(2, 72, 40, 32, 1, 2, 30), (2, 136, 64, 12, 1, 3, 24),
                                             (3, 4104, 64, 8, 2, 4, 12)])
 def test_fused_path_odd_shapes(L, d, ff, n, K, M, T):
