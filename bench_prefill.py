@@ -1,8 +1,8 @@
 #!/usr/bin/env python
-"""Prefill (f4) benchmark: one Mixtral-8x7B-shaped MoE layer over a prompt of T tokens,
-expert FFN as two tcgen05 tensor-core GEMMs per distinct routed expert.
+"""Prefill (f4) benchmark: one MoE layer of a BASELINE shape (default Mixtral-8x7B) over a
+prompt of T tokens, expert FFN as two tcgen05 tensor-core GEMMs per distinct routed expert.
 
-    python bench_prefill.py [--tokens 128,512,2048,4096] [--reps 20]
+    python bench_prefill.py [--shape mixtral-8x7b|phi-3.5-moe|mixtral-8x22b] [--tokens 128,512,2048,4096] [--reps 20]
 
 Prints one JSON line per T: tokens/s, the two GEMMs' TFLOP/s against the measured bf16
 dense peak (MEASURED_PEAKS.json), the weight-byte roofline (each expert's weights are read
@@ -26,6 +26,7 @@ import inputs  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="mixtral-8x7b", choices=["mixtral-8x7b", "phi-3.5-moe", "mixtral-8x22b"])
     ap.add_argument("--tokens", default="128,512,2048,4096")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--check", type=int, default=4, help="tokens checked against the oracle per T")
@@ -37,7 +38,7 @@ def main():
 
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         peaks = json.load(f)
-    c = inputs.CONFIGS["mixtral-8x7b"]
+    c = inputs.CONFIGS[args.shape]
     d, ff, n, K = c["d"], c["ff"], c["n"], c["K"]
     hm = harness.host_model(1, d, ff, n, K)
     dev = torch.device("cuda", 0)
@@ -85,7 +86,7 @@ def main():
             r = oracle.decode(x[t:t + 1], hm.gates, experts, N=1, M=n, K=K, warm_start=True)
             errs.append(float(np.abs(ybuf[t] - r.y[0, 0]).max() / np.abs(r.y[0, 0]).max()))
         peak = float(peaks["bf16_tflops"])
-        line = {"workload": "prefill: one Mixtral-8x7B-shaped MoE layer (d=4096, ff=14336, 8 experts top-2), M=8 warm",
+        line = {"workload": f"prefill: one {args.shape}-shaped MoE layer (d={d}, ff={ff}, {n} experts top-{K}), M={n} warm",
                 "T": T, "ms": ms, "tokens_per_s": T / (ms * 1e-3), "distinct_experts": distinct,
                 "tflops_total": (flops_g1 + flops_g2) / (ms * 1e-3) / 1e12,
                 "gemm_swiglu": {"ms": g1, "tflops": flops_g1 / (g1 * 1e-3) / 1e12,
