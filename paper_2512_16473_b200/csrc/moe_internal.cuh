@@ -187,11 +187,14 @@ struct TcArgs {
   float* y;                    // DOWN: y [T][d]
   const PrefillPlan* plan;     // SWIGLU / DOWN
   const uint32_t* ready;       // landed fill generation per slot
+  int mt_c2;                   // >0: both m-tiles-per-tile variants are launched and each exits
+                               // unless the exact tile counts pick it (cost of a 2-m-tile tile
+                               // = mt_c2/100 of a 1-m-tile one); 0: this variant runs
 };
 cudaError_t preload_tc_kernels();
 cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s);
-cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, cudaStream_t s);
-cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, cudaStream_t s);
+cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, int mt, cudaStream_t s);
+cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, int mt, cudaStream_t s);
 void launch_expert_gateup(const ExpertArgs& a, cudaStream_t s, int num_sms);
 void launch_expert_down(const ExpertArgs& a, cudaStream_t s, int num_sms);
 void launch_write_ready(uint32_t* ready, int slot, uint32_t gen, cudaStream_t s);

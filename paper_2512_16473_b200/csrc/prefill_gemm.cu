@@ -131,6 +131,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.mt_c2 > 0) {
+    // the routing (rows per expert) is only known here: estimate both variants as whole
+    // waves of the persistent grid times the tile cost, and run only the cheaper one
+    const int g = (int)gridDim.x;
+    const int w1 = (num_tiles<1>(p, BN) + g - 1) / g, w2 = (num_tiles<2>(p, BN) + g - 1) / g;
+    const int pick = 100 * w1 < p.mt_c2 * w2 ? 1 : 2;
+    if (pick != MT) return;
+  }
   const int ntiles = num_tiles<MT>(p, BN);
   if ((int)blockIdx.x >= ntiles) return;
   const int ktiles = p.K / BK;
@@ -315,6 +323,8 @@ cudaError_t preload_tc_kernels() {
   cudaError_t e = preload_tc<128, 1, 1>();
   if (e == cudaSuccess) e = preload_tc<128, 2, kMtSwiglu>();
   if (e == cudaSuccess) e = preload_tc<256, 1, kMtDown>();
+  if (e == cudaSuccess) e = preload_tc<128, 2, 1>();
+  if (e == cudaSuccess) e = preload_tc<256, 1, 1>();
   return e;
 }
 
@@ -324,16 +334,35 @@ cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s) {  // C = A B^T, BN
   return launch_tc<128, 1, 1>(p, ((p.N + 127) / 128) * ((p.M + BM - 1) / BM), sms, s);
 }
 
-cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, cudaStream_t s) {
+// mt = m-tiles per CTA tile (1 or 2, forced): one m-tile per tile gives twice the tiles, which
+// fills the 148 SMs better when a short prompt leaves few (expert, m-tile group, n tile) tiles.
+// mt = 0 (auto): both variants launched, the kernels pick on the device from the exact tile
+// counts (the one not picked exits before touching shared memory or TMEM). Tile costs relative
+// to a 1-m-tile tile, measured at T = 8192 (many waves): SwiGLU 1.7, down 1.95.
+static constexpr int kC2Swiglu = 170, kC2Down = 195;
+
+cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, int mt, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return launch_tc<128, 2, kMtSwiglu>(p, ((p.N + 127) / 128) * max_mtiles, sms, s);
+  const int tiles = ((p.N + 127) / 128) * max_mtiles;
+  TcArgs q = p;
+  q.mt_c2 = mt == 0 ? kC2Swiglu : 0;
+  cudaError_t e = cudaSuccess;
+  if (mt != 2) e = launch_tc<128, 2, 1>(q, tiles, sms, s);
+  if (e == cudaSuccess && mt != 1) e = launch_tc<128, 2, kMtSwiglu>(q, tiles, sms, s);
+  return e;
 }
 
-cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, cudaStream_t s) {
+cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, int mt, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return launch_tc<256, 1, kMtDown>(p, ((p.N + 255) / 256) * max_mtiles, sms, s);
+  const int tiles = ((p.N + 255) / 256) * max_mtiles;
+  TcArgs q = p;
+  q.mt_c2 = mt == 0 ? kC2Down : 0;
+  cudaError_t e = cudaSuccess;
+  if (mt != 2) e = launch_tc<256, 1, 1>(q, tiles, sms, s);
+  if (e == cudaSuccess && mt != 1) e = launch_tc<256, 1, kMtDown>(q, tiles, sms, s);
+  return e;
 }
 
 }  // namespace moe

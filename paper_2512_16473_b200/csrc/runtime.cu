@@ -932,6 +932,17 @@ MOE_API moe_status moe_layer_forward(moe_ctx* c, int32_t layer, const void* x, f
   return forward_impl(c, layer, x, y, (cudaStream_t)stream);
 }
 
+// m-tiles per CTA tile of the prefill GEMMs: 0 = chosen on the device from the exact tile
+// counts (prefill_gemm.cu); MOE_PREFILL_MT=1|2 forces one variant (A/B runs).
+static int prefill_mt() {
+  static const int forced = [] {
+    const char* e = getenv("MOE_PREFILL_MT");
+    const int v = e ? atoi(e) : 0;
+    return v == 1 || v == 2 ? v : 0;
+  }();
+  return forced;
+}
+
 MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, float* y, int32_t T, void* stream) {
   if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
   if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
@@ -1017,6 +1028,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   CUDA_TRY(launch_prefill_gather((const uint16_t*)x, c->d, c->d_plan, c->d_xg, rows_cap, s));
   // ---- tensor-core expert FFN: GEMM1 (SwiGLU) then GEMM2 (down + combine)
   const int max_mtiles = rows_cap / 128;
+  const int mt = prefill_mt();
   TcArgs ta;
   memset(&ta, 0, sizeof(ta));
   ta.d = c->d; ta.ffr = c->ffr; ta.ldh = c->ffr;
@@ -1028,7 +1040,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   ta.N = c->ffr; ta.K = c->d;
   ta.H = reinterpret_cast<__nv_bfloat16*>(c->d_hg);
   prof_begin(c, 1, s, &pe);
-  CUDA_TRY(launch_tc_swiglu(ta, max_mtiles, s));
+  CUDA_TRY(launch_tc_swiglu(ta, max_mtiles, mt, s));
   prof_end(c, s, &pe);
   ta.mode = TC_MODE_DOWN;
   ta.mapA = c->map_hg;
@@ -1036,7 +1048,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   ta.N = c->d; ta.K = c->ffr;
   ta.y = y;
   prof_begin(c, 2, s, &pe);
-  CUDA_TRY(launch_tc_down(ta, max_mtiles, s));
+  CUDA_TRY(launch_tc_down(ta, max_mtiles, mt, s));
   prof_end(c, s, &pe);
   if (c->P > 1) {
     prof_begin(c, 3, s, &pe);
