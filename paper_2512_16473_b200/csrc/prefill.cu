@@ -39,20 +39,23 @@ struct PfScratch {
   int nnew;
 };
 
-// (1) one warp per token: logits z = Wg x_t, top-K by (z desc, index asc), softmax over the
-//     K in rank order (exactly the decode router's arithmetic order for the softmax), first
-//     access key and entry count per expert.
+// (1) one CTA per token: logits z = Wg x_t (warp w takes experts w, w+8, ...: each logit is
+//     a lane-strided sum then a shuffle tree, so 8 independent chains per token instead of n
+//     serial ones), then warp 0 takes top-K by (z desc, index asc), softmax over the K in rank
+//     order (exactly the decode router's arithmetic order for the softmax), first access key
+//     and entry count per expert.
 __global__ void __launch_bounds__(256) prefill_route_kernel(const PrefillArgs a, const uint16_t* __restrict__ Wg,
                                                             const uint16_t* __restrict__ x, int d) {
-  const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  __shared__ float zs[MOE_MAX_EXPERTS];
+  const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (t >= a.T) return;
   PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
   const int n = a.n, K = a.K;
   const int4* xv = reinterpret_cast<const int4*>(x + (size_t)t * d);
-  float z = -INFINITY;
-  for (int e = 0; e < n; ++e) {
+  for (int e = warp; e < n; e += 8) {
     const int4* wr = reinterpret_cast<const int4*>(Wg + (size_t)e * d);
     float acc = 0.f;
+#pragma unroll 4
     for (int c = lane; c < (d >> 3); c += 32) {
       const int4 w4 = __ldg(wr + c), x4 = __ldg(xv + c);
       acc = fmaf(bfl(w4.x), bfl(x4.x), acc);
@@ -66,8 +69,11 @@ __global__ void __launch_bounds__(256) prefill_route_kernel(const PrefillArgs a,
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == e) z = acc;
+    if (lane == 0) zs[e] = acc;
   }
+  __syncthreads();
+  if (warp != 0) return;
+  const float z = lane < n ? zs[lane] : -INFINITY;
   bool taken = lane >= n;
   int myS = -1;
   float myZ = 0.f;
@@ -308,7 +314,7 @@ cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const
   if (e == cudaSuccess) e = cudaMemsetAsync(a.scratch, 0x7f, sizeof(int) * MOE_MAX_EXPERTS, s);
   if (e != cudaSuccess) return e;
   const int blocks = (a.T + 7) / 8;
-  prefill_route_kernel<<<blocks, 256, 0, s>>>(a, Wg, x, d);
+  prefill_route_kernel<<<a.T, 256, 0, s>>>(a, Wg, x, d);
   prefill_plan_kernel<<<1, 32, 0, s>>>(a);
   prefill_access_kernel<<<blocks, 256, 0, s>>>(a);
   prefill_lists_kernel<<<a.n, 1024, 0, s>>>(a);
