@@ -107,36 +107,48 @@ __global__ void __launch_bounds__(256) prefill_route_kernel(const PrefillArgs a,
 // (2) one CTA: which experts are resident, ways for the first-touch experts (lowest invalid
 //     way, in access order — R10 with M = n), fills (mailbox), plan blocks, directory tags.
 __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
+  // the walk below is serial and short (n, M <= 32): its inputs are staged in shared memory
+  // by parallel loads first, so it does not pay a dependent global-memory round trip per step
+  __shared__ int cnt[MOE_MAX_EXPERTS], first[MOE_MAX_EXPERTS], way[MOE_MAX_EXPERTS], tag[MOE_MAX_EXPERTS];
+  __shared__ uint32_t gen[MOE_MAX_EXPERTS];
   PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
-  if (threadIdx.x != 0) return;
-  const int n = a.n, M = a.M;
-  int tag[MOE_MAX_EXPERTS];
-  for (int w = 0; w < M; ++w) tag[w] = a.tag[w];
+  const int n = a.n, M = a.M, i = threadIdx.x;
+  if (i < n) {
+    cnt[i] = sc->cnt[i];
+    first[i] = sc->first[i];
+  }
+  if (i < M) {
+    tag[i] = a.tag[i];
+    gen[i] = a.gen[a.slot_base + i];
+  }
+  __syncthreads();
+  if (i != 0) return;
   sc->clock0 = *a.clock;
   int nnew = 0;
+  int isnew[MOE_MAX_EXPERTS];
   for (int e = 0; e < n; ++e) {
-    sc->way[e] = -1;
-    sc->isnew[e] = 0;
-    for (int w = 0; w < M; ++w)
-      if (tag[w] == e) sc->way[e] = w;
+    way[e] = -1;
+    isnew[e] = 0;
   }
+  for (int w = 0; w < M; ++w)
+    if (tag[w] >= 0 && tag[w] < n) way[tag[w]] = w;
   // first-touch experts in access order (selection by first key; n <= 32)
-  int done[MOE_MAX_EXPERTS];
-  for (int e = 0; e < n; ++e) done[e] = 0;
+  uint32_t done = 0;
   while (true) {
     int best = -1;
     for (int e = 0; e < n; ++e)
-      if (!done[e] && sc->cnt[e] > 0 && sc->way[e] < 0 && (best < 0 || sc->first[e] < sc->first[best])) best = e;
+      if (!((done >> e) & 1u) && cnt[e] > 0 && way[e] < 0 && (best < 0 || first[e] < first[best])) best = e;
     if (best < 0) break;
-    done[best] = 1;
+    done |= 1u << best;
     int v = -1;
     for (int w = 0; w < M && v < 0; ++w)
       if (tag[w] == -1) v = w;
     tag[v] = best;
-    sc->way[best] = v;
-    sc->isnew[best] = 1;
+    way[best] = v;
+    isnew[best] = 1;
     sc->newrank[best] = nnew;
-    const uint32_t g = a.gen[a.slot_base + v] + 1u;
+    const uint32_t g = gen[v] + 1u;
+    gen[v] = g;
     a.gen[a.slot_base + v] = g;
     a.tag[v] = best;
     a.mail->expert[nnew] = best;
@@ -150,13 +162,15 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
   // plan: blocks in expert id order, 128-row padded
   int nb = 0, off = 0, mt = 0;
   for (int e = 0; e < n; ++e) {
-    if (!sc->cnt[e]) continue;
-    const int tiles = (sc->cnt[e] + 127) / 128;
+    sc->way[e] = way[e];
+    sc->isnew[e] = isnew[e];
+    if (!cnt[e]) continue;
+    const int tiles = (cnt[e] + 127) / 128;
     a.plan->row_off[nb] = off;
     a.plan->mt_pref[nb] = mt;
-    a.plan->slot[nb] = a.slot_base + sc->way[e];
-    a.plan->gen[nb] = a.gen[a.slot_base + sc->way[e]];
-    a.plan->wait[nb] = sc->isnew[e];
+    a.plan->slot[nb] = a.slot_base + way[e];
+    a.plan->gen[nb] = gen[way[e]];
+    a.plan->wait[nb] = isnew[e];
     sc->offs[e] = off;
     off += tiles * 128;
     mt += tiles;
@@ -315,7 +329,7 @@ cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const
   if (e != cudaSuccess) return e;
   const int blocks = (a.T + 7) / 8;
   prefill_route_kernel<<<a.T, 256, 0, s>>>(a, Wg, x, d);
-  prefill_plan_kernel<<<1, 32, 0, s>>>(a);
+  prefill_plan_kernel<<<1, 64, 0, s>>>(a);
   prefill_access_kernel<<<blocks, 256, 0, s>>>(a);
   prefill_lists_kernel<<<a.n, 1024, 0, s>>>(a);
   return cudaGetLastError();
