@@ -194,10 +194,17 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
 //     (every access increments the clock: hits of the token first, then its misses, each
 //     in rank order — the decode router's order).
 __global__ void __launch_bounds__(256) prefill_access_kernel(const PrefillArgs a) {
+  // per-CTA aggregation in shared memory (8 tokens), then one global atomic per counter and
+  // per touched expert: the global atomics no longer serialise on a handful of addresses
+  __shared__ unsigned long long cs[6];  // accesses, >=1 hit, all-K hit, hits, misses
+  __shared__ unsigned long long lastc_s[MOE_MAX_EXPERTS];
   const int t = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const PfScratch* sc = reinterpret_cast<const PfScratch*>(a.scratch);
   PfScratch* scw = reinterpret_cast<PfScratch*>(a.scratch);
   const int K = a.K;
+  if (threadIdx.x < 6) cs[threadIdx.x] = 0ull;
+  if (threadIdx.x < MOE_MAX_EXPERTS) lastc_s[threadIdx.x] = 0ull;
+  __syncthreads();
   int e = -1, hit = 0;
   if (t < a.T && lane < K) {
     e = a.rt_e[(size_t)t * K + lane];
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(256) prefill_access_kernel(const PrefillArgs a
   if (t < a.T && lane < K) {
     const int pos = hit ? __popc(hm & ((1u << lane) - 1u)) : __popc(hm) + __popc(mm & ((1u << lane) - 1u));
     if (a.policy == MOE_POLICY_LRU)
-      atomicMax(&scw->lastc[e], sc->clock0 + (unsigned long long)t * K + pos + 1);
+      atomicMax(&lastc_s[e], sc->clock0 + (unsigned long long)t * K + pos + 1);
     const long long ti = a.trace_idx + (long long)t * K + lane;
     if (ti < a.trace_cap) {
       moe_access_record rec;
@@ -225,18 +232,27 @@ __global__ void __launch_bounds__(256) prefill_access_kernel(const PrefillArgs a
       a.trace[ti] = rec;
     }
   }
-  // counters: one reduction per warp
   if (lane == 0 && t < a.T) {
     const int nh = __popc(hm);
+    atomicAdd(&cs[0], 1ull);
+    if (nh > 0) atomicAdd(&cs[1], 1ull);
+    if (nh == K) atomicAdd(&cs[2], 1ull);
+    if (nh) atomicAdd(&cs[3], (unsigned long long)nh);
+    if (K - nh) atomicAdd(&cs[4], (unsigned long long)(K - nh));
+  }
+  __syncthreads();
+  if (threadIdx.x < MOE_MAX_EXPERTS && lastc_s[threadIdx.x])
+    atomicMax(&scw->lastc[threadIdx.x], lastc_s[threadIdx.x]);
+  if (threadIdx.x == 0) {
     DevStats* s = a.stats;
-    atomicAdd(&s->accesses, 1ull);
-    if (nh > 0) atomicAdd(&s->at_least_one_hit, 1ull);
-    if (nh == K) atomicAdd(&s->all_k_hit, 1ull);
-    if (nh) atomicAdd(&s->expert_hits, (unsigned long long)nh);
-    if (K - nh) {
-      atomicAdd(&s->expert_misses, (unsigned long long)(K - nh));
-      atomicAdd(&s->fetches, (unsigned long long)(K - nh));
-      atomicAdd(&s->fetch_bytes, (unsigned long long)(K - nh) * (unsigned long long)a.slot_bytes);
+    if (cs[0]) atomicAdd(&s->accesses, cs[0]);
+    if (cs[1]) atomicAdd(&s->at_least_one_hit, cs[1]);
+    if (cs[2]) atomicAdd(&s->all_k_hit, cs[2]);
+    if (cs[3]) atomicAdd(&s->expert_hits, cs[3]);
+    if (cs[4]) {
+      atomicAdd(&s->expert_misses, cs[4]);
+      atomicAdd(&s->fetches, cs[4]);
+      atomicAdd(&s->fetch_bytes, cs[4] * (unsigned long long)a.slot_bytes);
     }
   }
 }
