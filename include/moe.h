@@ -128,9 +128,20 @@ typedef enum {
  *    stream "for future access"; the result comes back on a second (activation) stream and
  *    the expert kernel adds it. Layers beyond coverage are computed on the host only
  *    (P:201). A later hit on a slot whose post-fetch has not landed waits for it
- *    (counted in hit_under_fill). Requires K <= 2 (fused expert kernel). */
+ *    (counted in hit_under_fill). Requires K <= 2 (fused expert kernel).
+ *  MOE_MISS_PULL (B200 design, no host thread on the path): the call's own kernel copies a
+ *    missed expert from the pinned backing store into its victim slot (or staging slot)
+ *    with SM loads over PCIe — every CTA pulls a 1/grid share of the blob, a grid-wide
+ *    counter orders the copy before the expert GEMVs read the slot — and then computes it
+ *    on the GPU. Same cache semantics, counters and trace as MOE_MISS_FETCH (a miss is
+ *    filled before its own call computes it: hit_under_fill = 0). Nothing waits on a host
+ *    thread or a copy engine, so a call behaves like any stream-ordered kernel under
+ *    serialising tools (ncu replay, compute-sanitizer) and inside CUDA graph capture.
+ *    Requires every expert blob to be device-accessible pinned memory (cudaHostAlloc,
+ *    cudaHostRegister; checked in cache_configure: MOE_ERR_UNSUPPORTED otherwise). */
 #define MOE_MISS_FETCH 0
 #define MOE_MISS_HOST_COMPUTE 1
+#define MOE_MISS_PULL 2
 
 typedef struct {
   int64_t cache_bytes;
@@ -141,7 +152,7 @@ typedef struct {
   uint64_t seed; /* STATIC_RANDOM only: seed of the resident draw */
   void* pool;
   int64_t pool_bytes;
-  int32_t miss_mode;    /* MOE_MISS_FETCH | MOE_MISS_HOST_COMPUTE */
+  int32_t miss_mode;    /* MOE_MISS_FETCH | MOE_MISS_HOST_COMPUTE | MOE_MISS_PULL */
   int32_t host_threads; /* host-compute threads (<= 0: all hardware threads) */
 } moe_cache_config;
 
@@ -172,7 +183,7 @@ MOE_API moe_status moe_layer_forward(moe_ctx* ctx, int32_t layer, const void* x,
  * per distinct routed expert as two tcgen05 tensor-core GEMMs (SwiGLU fused into the first,
  * the gate-weighted combine into the second; h rounded to bf16 between them, so outputs
  * differ from the decode path by up to ~1e-3 relative). Requirements (else
- * MOE_ERR_UNSUPPORTED): full associativity (ways == n), layer covered, MOE_MISS_FETCH,
+ * MOE_ERR_UNSUPPORTED): full associativity (ways == n), layer covered, MOE_MISS_FETCH or MOE_MISS_PULL,
  * K <= 2, d % 64 == 0, (ff/P) % 128 == 0. First-touch misses are fetched into their slots. */
 MOE_API moe_status moe_layer_prefill(moe_ctx* ctx, int32_t layer, const void* x, float* y, int32_t T, void* stream);
 
@@ -188,7 +199,7 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* ctx, int32_t layer, const uin
  *  expert_misses includes coverage_misses (layers >= N). fetches / fetch_bytes count
  *  host->device expert copies (one per miss, including staging fills).
  *  hit_under_fill: hits on a slot whose fill had not landed yet at probe time (timing
- *  dependent — not part of the bit-exact contract; always 0 with MOE_MISS_FETCH, where a
+ *  dependent — not part of the bit-exact contract; always 0 with MOE_MISS_FETCH / PULL, where a
  *  miss is filled before its own call computes it).
  *  host_computed: experts computed by the host cores (MOE_MISS_HOST_COMPUTE). In that mode
  *  fetches count post-fetches (covered misses only). */

@@ -12,10 +12,10 @@ import ctypes
 import numpy as np
 
 from . import _abi
-from ._abi import (MISS_FETCH, MISS_HOST_COMPUTE, POLICY_FIFO, POLICY_LRU, POLICY_STATIC_RANDOM, PROF_KINDS,
+from ._abi import (MISS_FETCH, MISS_HOST_COMPUTE, MISS_PULL, POLICY_FIFO, POLICY_LRU, POLICY_STATIC_RANDOM, PROF_KINDS,
                    RECORD_DTYPE, STAT_FIELDS)
 
-__all__ = ["Moe", "MoeError", "PinnedBuffer", "MISS_FETCH", "MISS_HOST_COMPUTE", "host_expert_ffn", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
+__all__ = ["Moe", "MoeError", "PinnedBuffer", "MISS_FETCH", "MISS_HOST_COMPUTE", "MISS_PULL", "host_expert_ffn", "POLICY_LRU", "POLICY_FIFO", "POLICY_STATIC_RANDOM", "RECORD_DTYPE",
            "STAT_FIELDS", "slot_bytes", "blob_views", "lib", "nccl_unique_id", "PROF_KINDS", "tp_connect_local"]
 
 _lib = None

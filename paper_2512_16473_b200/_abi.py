@@ -54,7 +54,7 @@ class CacheGeometry(ctypes.Structure):
 
 STAT_FIELDS = ("accesses", "at_least_one_hit", "all_k_hit", "expert_hits", "expert_misses",
                "coverage_misses", "evictions", "fetches", "fetch_bytes", "hit_under_fill", "host_computed")
-MISS_FETCH, MISS_HOST_COMPUTE = 0, 1
+MISS_FETCH, MISS_HOST_COMPUTE, MISS_PULL = 0, 1, 2
 
 
 class LayerStats(ctypes.Structure):

@@ -37,6 +37,7 @@
 
 #include "moe_internal.cuh"
 #include "ptx.cuh"
+#include "pull.cuh"
 #include "route_core.cuh"
 
 namespace moe {
@@ -52,6 +53,8 @@ constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
 constexpr int kTsPerCta = 40;             // debug timestamps per CTA (MOE_DEBUG_TS)
 constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stage
+constexpr int kPullBar = 14;              // named barrier: consumers' MOE_MISS_PULL copies done
+constexpr int kPullCtr = 16 * 8;          // bar[] word counting CTAs done pulling (every call adds G)
 
 // Packed fp32 FMA (sm_100: FFMA2): acc.{x,y} += a.{x,y} * b.{x,y}
 __device__ __forceinline__ float2 ffma2(const float2 a, const float2 b, const float2 c) {
@@ -115,6 +118,16 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// spin until *p >= target (acquire); 60 s -> trap
+__device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target) {
+  if (ld_acquire_u64(p) >= target) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_u64(p) < target) {
+    __nanosleep(64);
+    if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+  }
 }
 
 // f3: fused tensor-parallel reduction of y over the ranks' exchange buffers (moe.h,
@@ -236,7 +249,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ const uint8_t* sbase[kMaxFusedK];
   __shared__ float swgt[kMaxFusedK];
-  __shared__ int swait[kMaxFusedK], shost[kMaxFusedK], sslot[kMaxFusedK], sorder[kMaxFusedK];
+  __shared__ int swait[kMaxFusedK], shost[kMaxFusedK], sslot[kMaxFusedK], sorder[kMaxFusedK], sexp[kMaxFusedK];
   __shared__ uint32_t sgen[kMaxFusedK];
   __shared__ int snseg, smerged;
   __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
@@ -393,6 +406,23 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
     if (pm && threadIdx.x == 32) pm[2] = clock64();
     named_bar_arrive(kRouteBar, nthr + 32);  // partial logits ready; on to phase A
+    if (f.r.miss_mode == MOE_MISS_PULL) {
+      // MOE_MISS_PULL: this CTA's share of every missed expert's blob, host store -> slot,
+      // before any phase-A row is consumed (the producer streams resident experts meanwhile
+      // and waits for every CTA's share before its first row of a pulled expert)
+      mbar_wait(&rbar, 0);
+      bool any = false;
+      for (int r = 0; r < K; ++r) {
+        if (!swait[r] || shost[r]) continue;
+        any = true;
+        long long u0, u1;
+        pull_share(a.slot_bytes, b, G, &u0, &u1);
+        pull_copy(const_cast<uint8_t*>(sbase[r]), ra.hblob[sexp[r]], u0, u1, ctid, nthr);
+      }
+      if (any) named_bar_sync(kPullBar, nthr);  // (uniform: every consumer read the same route)
+    }
+    // one arrival per CTA and call, in every mode (the counter's target is (calls + 1) * G)
+    if (ctid == 0) red_release_add_u64(f.bar + kPullCtr, 1ull);
   } else if (warp == kRouterWarp) {
     // ---------------------------------------------------------------- router warp
     // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects.
@@ -400,7 +430,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // While the consumers run the gate GEMV: where each expert sits in the set (lane e:
     // its way and that way's generation, from the pre-access directory), so an all-hit
     // route can be published straight from the logits.
-    const bool fast = ra.covered && ra.miss_mode == MOE_MISS_FETCH;
+    const bool fast = ra.covered && ra.miss_mode != MOE_MISS_HOST_COMPUTE;
     int way_of = -1;
     uint32_t gen_of = 0u;
     if (fast)
@@ -435,6 +465,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           shost[rank] = 0;
           sbase[rank] = a.pool + (long long)slot * a.slot_bytes;
           sorder[rank] = rank;
+          sexp[rank] = lane;
         }
         if (lane == 0) {
           snseg = K;
@@ -453,6 +484,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         swait[lane] = lr.wait;
         shost[lane] = lr.host;
         sbase[lane] = a.pool + (long long)lr.slot * a.slot_bytes;
+        sexp[lane] = lr.expert;
       }
       // device-computed experts in processing order: resident ones first, then the ones
       // whose fill may still be in flight (rank order within each)
@@ -477,12 +509,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (!published) publish(lr);
     if (lane < K) swgt[lane] = lr.w;       // gate weights: needed from phase B on
     mbar_arrive(&wbar);
-    // miss mailbox entry (host-mapped): payload, system fence, seq (the fetch thread's
-    // trigger)
-    if (lane == 0 && writer && nmiss) {
-      __threadfence_system();
-      ra.mail->seq = ra.seq;
-    }
+    // miss mailbox entry (host-mapped: seq after its payload, P:200's trigger) and progress word
+    if (lane == 0 && writer) publish_progress(ra, nmiss);
     griddep_launch_dependents();
     __syncwarp();                          // (sorder / smerged written by other router lanes)
     if (lane == 0 && smerged) {
@@ -533,7 +561,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* base = sbase[r];
-        if (swait[r]) wait_ready(a.ready, sslot[r], sgen[r]);  // fill of this slot still in flight
+        if (swait[r]) {  // fill of this slot still in flight (FETCH) / being pulled by every CTA (PULL)
+          if (ra.miss_mode == MOE_MISS_PULL) wait_counter(f.bar + kPullCtr, (f.calls + 1) * (unsigned long long)G);
+          else wait_ready(a.ready, sslot[r], sgen[r]);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic/DMA writes -> bulk reads
+        }
         unsigned* cA = ctr + r;
         auto issue_a = [&](int j) {
           const int s = t % NS;
@@ -610,10 +642,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
         if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
         marker_b(kEnd);
-        if (b == 0) {
-          __threadfence_system();
-          *a.last_seq = a.seq;
-        }
         return;
       }
       const RowSched sbk = make_sched(d, b, G, f.pctB);
@@ -648,13 +676,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       }
       if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
       marker_b(kEnd);
-      // publish the call's progress to the host fetch thread (PCIe write overlaps the tail);
-      // the system fence orders this call's mailbox entry (written by the routing warp
-      // before the CTA barrier) before it
-      if (b == 0) {
-        __threadfence_system();
-        *a.last_seq = a.seq;
-      }
     }
     return;
   }
@@ -821,8 +842,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (!shost[r]) continue;
     if (cw == 0 && lane == 0) {
       // every CTA zeroed its slice of y before publishing on bar[r] (release)
-      while (ld_acquire_u64(f.bar + 16 * r) < bar_target) {
-      }
+      wait_counter(f.bar + 16 * r, bar_target);
       const uint32_t want = (uint32_t)a.seq;
       const unsigned long long t0 = globaltimer();
       unsigned ns = 256;

@@ -152,7 +152,6 @@ __global__ void __launch_bounds__(kThreads) expert_down_kernel(const ExpertArgs 
     }
     if (lane == 0) a.y[c] = y;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.last_seq = a.seq;  // progress word for the fetch thread
 }
 
 }  // namespace

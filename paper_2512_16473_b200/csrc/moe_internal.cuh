@@ -72,6 +72,8 @@ struct RouteArgs {
   unsigned long long seq;
   long long slot_bytes;
   unsigned long long* sts;  // debug (MOE_DEBUG_TS): this call's step-timestamp record, or nullptr
+  const uint8_t* const* hblob;  // [n] device-accessible pinned host blobs of this layer (MOE_MISS_PULL)
+  volatile unsigned long long* last_seq;  // host-mapped progress word (CTA 0's router publishes seq)
 };
 
 struct ExpertArgs {
@@ -148,11 +150,12 @@ struct PrefillPlan {
   int slot[kPrefillMaxBlk];
   uint32_t gen[kPrefillMaxBlk];
   int wait[kPrefillMaxBlk];   // 1: the slot is filled by this call -> wait for gen
+  int expert[kPrefillMaxBlk]; // expert of each block
   int* tok;      // [rows_cap] token of each gathered row (-1 = padding)
   float* wrow;   // [rows_cap] gate weight of that token for the block's expert
 };
 struct PrefillArgs {
-  int T, n, K, M, layer, policy;
+  int T, n, K, M, layer, policy, miss_mode;
   int32_t* tag;                // set of the layer
   unsigned long long* stamp;
   int slot_base;
@@ -166,10 +169,29 @@ struct PrefillArgs {
   uint32_t token0;
   Mail* mail;
   unsigned long long seq;
+  volatile unsigned long long* last_seq;  // host-mapped progress word (the plan kernel publishes seq)
   long long slot_bytes;
   PrefillPlan* plan;
   void* scratch;               // prefill_scratch_bytes() of device scratch
 };
+// MOE_MISS_PULL outside the fused kernel (split decode path, prefill): copy the listed
+// blobs (flag[i] != 0, i < *count) from the pinned host store into their slots, then
+// publish ready[slot[i]] = gen[i] (pull.cu).
+struct PullJob {
+  const int32_t* count;
+  const int32_t* expert;
+  const int32_t* slot;
+  const uint32_t* gen;
+  const int32_t* flag;
+  const uint8_t* const* hblob;  // [n] blobs of the layer
+  uint8_t* pool;
+  long long slot_bytes;
+  uint32_t* ready;
+  unsigned* done;               // completion counter (zero between launches)
+};
+cudaError_t preload_pull_kernels();
+cudaError_t launch_pull(const PullJob& j, int grid, cudaStream_t s);
+
 size_t prefill_scratch_bytes();
 cudaError_t preload_prefill_kernels();
 cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const uint16_t* x, int d, cudaStream_t s);
@@ -187,6 +209,7 @@ struct TcArgs {
   float* y;                    // DOWN: y [T][d]
   const PrefillPlan* plan;     // SWIGLU / DOWN
   const uint32_t* ready;       // landed fill generation per slot
+  int num_sms;                 // persistent grid size (0: the current device's SM count)
   int mt_c2;                   // >0: both m-tiles-per-tile variants are launched and each exits
                                // unless the exact tile counts pick it (cost of a 2-m-tile tile
                                // = mt_c2/100 of a 1-m-tile one); 0: this variant runs

@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
   for (int w = 0; w < M; ++w)
     if (tag[w] >= 0 && tag[w] < n) way[tag[w]] = w;
   // first-touch experts in access order (selection by first key; n <= 32)
+  const bool mailbox = a.miss_mode != MOE_MISS_PULL;  // PULL: a pull kernel fills the slots
   uint32_t done = 0;
   while (true) {
     int best = -1;
@@ -151,11 +152,13 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
     gen[v] = g;
     a.gen[a.slot_base + v] = g;
     a.tag[v] = best;
-    a.mail->expert[nnew] = best;
-    a.mail->slot[nnew] = a.slot_base + v;
-    a.mail->gen[nnew] = g;
-    a.mail->rank[nnew] = 0;
-    a.mail->postfetch[nnew] = 1;
+    if (mailbox) {
+      a.mail->expert[nnew] = best;
+      a.mail->slot[nnew] = a.slot_base + v;
+      a.mail->gen[nnew] = g;
+      a.mail->rank[nnew] = 0;
+      a.mail->postfetch[nnew] = 1;
+    }
     ++nnew;
   }
   sc->nnew = nnew;
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
     a.plan->slot[nb] = a.slot_base + way[e];
     a.plan->gen[nb] = gen[way[e]];
     a.plan->wait[nb] = isnew[e];
+    a.plan->expert[nb] = e;
     sc->offs[e] = off;
     off += tiles * 128;
     mt += tiles;
@@ -180,13 +184,18 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
   a.plan->nblk = nb;
   a.plan->total_mtiles = mt;
   a.plan->rows = off;
-  if (nnew) {
+  // fills of the first-touch experts (mailbox: payload, system fence, seq) and the call's
+  // progress word, published here, as soon as the entry is final: every later step of the
+  // call may fail or be cancelled without leaving the fetch thread waiting for this seq
+  if (nnew && mailbox) {
     a.mail->layer = a.layer;
     a.mail->nmiss = nnew;
     a.mail->host = 0;
     __threadfence_system();
     a.mail->seq = a.seq;
+    __threadfence_system();
   }
+  *a.last_seq = a.seq;
 }
 
 // (3) one warp per token: hit/miss (pre-access partition: hit iff resident before the call

@@ -328,9 +328,19 @@ cudaError_t preload_tc_kernels() {
   return e;
 }
 
+// persistent grid size: the context's SM count (TcArgs.num_sms), else the current device's
+static int grid_sms(const TcArgs& p) {
+  if (p.num_sms > 0) return p.num_sms;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  return sms;
+}
+
 cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s) {  // C = A B^T, BN = 128
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = grid_sms(p);
   return launch_tc<128, 1, 1>(p, ((p.N + 127) / 128) * ((p.M + BM - 1) / BM), sms, s);
 }
 
@@ -342,8 +352,7 @@ cudaError_t launch_tc_plain(const TcArgs& p, cudaStream_t s) {  // C = A B^T, BN
 static constexpr int kC2Swiglu = 170, kC2Down = 195;
 
 cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, int mt, cudaStream_t s) {
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = grid_sms(p);
   const int tiles = ((p.N + 127) / 128) * max_mtiles;
   TcArgs q = p;
   q.mt_c2 = mt == 0 ? kC2Swiglu : 0;
@@ -354,8 +363,7 @@ cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, int mt, cudaStream
 }
 
 cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, int mt, cudaStream_t s) {
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = grid_sms(p);
   const int tiles = ((p.N + 255) / 256) * max_mtiles;
   TcArgs q = p;
   q.mt_c2 = mt == 0 ? kC2Down : 0;

@@ -232,6 +232,7 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
   const int nhuf = __popc(__ballot_sync(0xffffffffu, lane < K && myHit && myWait));
   const int npost = __popc(__ballot_sync(0xffffffffu, lane < K && myPost));
   const unsigned missmask = __ballot_sync(0xffffffffu, lane < K && !myHit);
+  const bool mailbox = a.miss_mode != MOE_MISS_PULL;  // PULL: the kernel fills the slots itself
   if (hostmode && missmask)  // ship x to host memory for the host-side expert computation
     for (int i = lane; i < (a.d >> 3); i += 32)
       reinterpret_cast<int4*>(a.xmail)[i] = reinterpret_cast<const int4*>(a.x)[i];
@@ -252,7 +253,7 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
       rec.weight = sW[lane];
       a.trace[a.trace_idx + lane] = rec;
     }
-    if (!myHit) {
+    if (!myHit && mailbox) {
       const int i = __popc(missmask & ((1u << lane) - 1u));
       a.mail->expert[i] = myS;
       a.mail->slot[i] = mySlot;
@@ -281,13 +282,28 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
     // hit_under_fill is 0 in FETCH mode by construction: a miss is filled before its own
     // call reads the slot, so no later access can find it still filling.
     if (nhuf) atomicAdd(&s->hit_under_fill, (unsigned long long)nhuf);
-    if (nmiss) {
+    if (nmiss && mailbox) {
       a.mail->layer = a.layer;
       a.mail->nmiss = nmiss;
       a.mail->host = hostmode;
     }
   }
   return nmiss;
+}
+
+// The writer's lane 0, after route_decide: the miss mailbox entry's seq (FETCH /
+// HOST_COMPUTE misses: payload, system fence, seq — the fetch thread's trigger), then
+// the call's progress word. progress >= seq tells the fetch thread that the entry of seq,
+// if any, is visible; without a miss nothing needs ordering, so the all-hit path issues no
+// system-scope fence (a fence at the end of the kernel delayed its completion, and with it
+// the next call's PDL wait, by ~2 us).
+__device__ __forceinline__ void publish_progress(const RouteArgs& a, int nmiss) {
+  if (nmiss && a.miss_mode != MOE_MISS_PULL) {
+    __threadfence_system();
+    a.mail->seq = a.seq;
+    __threadfence_system();
+  }
+  *a.last_seq = a.seq;
 }
 
 }  // namespace moe

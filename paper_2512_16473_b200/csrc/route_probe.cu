@@ -106,16 +106,8 @@ __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a
     a.sts[1] = ptx::globaltimer();
     a.sts[5] = clock64() - ck0;
   }
-  if (lane == 0) {
-    // Miss mailbox (host-mapped): an entry is written only when this call missed (payload,
-    // system fence, seq). The progress word is published by the expert kernels at their end
-    // (off this kernel's critical path): progress >= seq implies this kernel completed, so
-    // an entry for seq is visible if it exists.
-    if (nmiss) {
-      __threadfence_system();
-      a.mail->seq = a.seq;
-    }
-  }
+  // miss mailbox entry (host-mapped; FETCH / HOST_COMPUTE misses) and the progress word
+  if (lane == 0) publish_progress(a, nmiss);
 }
 
 __global__ void write_ready_kernel(uint32_t* ready, int slot, uint32_t gen) {

@@ -121,6 +121,9 @@ struct moe_ctx {
   // weights
   std::vector<const uint16_t*> blobs;
   std::vector<void*> registered;
+  const uint8_t** d_hblob = nullptr;  // [L*n] device-accessible aliases of the blobs (MOE_MISS_PULL)
+  bool hblob_ok = false;              // every blob is device-accessible pinned memory
+  unsigned* d_pull_done = nullptr;    // pull kernel completion counter (split path / prefill)
   uint16_t* d_gate = nullptr;
   // streams
   cudaStream_t fetch_stream = nullptr, own_stream = nullptr;
@@ -364,7 +367,14 @@ void free_cache(moe_ctx* c) {
 // Wait until every issued call's mailbox was consumed and the fetch stream drained.
 moe_status drain(moe_ctx* c) {
   if (c->any_call) CUDA_TRY(cudaEventSynchronize(c->done_ev));
-  while (c->consumed.load(std::memory_order_acquire) < c->issued.load()) std::this_thread::yield();
+  // every issued call has completed on the device, so its progress word is published: the
+  // fetch thread catches up within its polling period unless something is broken
+  const auto t0 = std::chrono::steady_clock::now();
+  while (c->consumed.load(std::memory_order_acquire) < c->issued.load()) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+      return fail(MOE_ERR_STATE, "fetch thread did not reach the last issued call within 60 s");
+    std::this_thread::yield();
+  }
   CUDA_TRY(cudaStreamSynchronize(c->fetch_stream));
   if (c->act_stream) CUDA_TRY(cudaStreamSynchronize(c->act_stream));
   if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
@@ -502,15 +512,34 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(preload_fused_kernels());
   INIT_TRY(preload_tc_kernels());
   INIT_TRY(preload_prefill_kernels());
+  INIT_TRY(preload_pull_kernels());
   INIT_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   c->blobs.assign(w->expert_blob, w->expert_blob + (size_t)L * n);
   if (!w->already_pinned) {
     for (auto* b : c->blobs) {
-      e = cudaHostRegister((void*)b, (size_t)c->slot_bytes, cudaHostRegisterDefault);
+      e = cudaHostRegister((void*)b, (size_t)c->slot_bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
       if (e == cudaSuccess) c->registered.push_back((void*)b);
       else if (e == cudaErrorHostMemoryAlreadyRegistered) cudaGetLastError();
       else return bail(fail(MOE_ERR_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e)));
     }
+  }
+  {
+    // device aliases of the pinned blobs, read by the kernels in MOE_MISS_PULL mode
+    std::vector<const uint8_t*> hb((size_t)L * n);
+    c->hblob_ok = true;
+    for (size_t i = 0; i < hb.size() && c->hblob_ok; ++i) {
+      void* dp = nullptr;
+      if (cudaHostGetDevicePointer(&dp, (void*)c->blobs[i], 0) != cudaSuccess || !dp || ((uintptr_t)dp & 15)) {
+        cudaGetLastError();
+        c->hblob_ok = false;
+      }
+      hb[i] = (const uint8_t*)dp;
+    }
+    INIT_TRY(cudaMalloc(&c->d_hblob, sizeof(const uint8_t*) * hb.size()));
+    if (c->hblob_ok)
+      INIT_TRY(cudaMemcpy(c->d_hblob, hb.data(), sizeof(const uint8_t*) * hb.size(), cudaMemcpyHostToDevice));
+    INIT_TRY(cudaMalloc(&c->d_pull_done, sizeof(unsigned)));
+    INIT_TRY(cudaMemset(c->d_pull_done, 0, sizeof(unsigned)));
   }
   const size_t gate_elems = (size_t)n * d;
   INIT_TRY(cudaMalloc(&c->d_gate, gate_elems * 2 * L));
@@ -632,6 +661,8 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   for (auto e : c->ev_free) cudaEventDestroy(e);
   free_cache(c);
   cudaFree(c->d_gate);
+  cudaFree(c->d_hblob);
+  cudaFree(c->d_pull_done);
   cudaFree(c->d_route);
   cudaFree(c->d_h);
   cudaFree(c->d_x_e2e);
@@ -678,8 +709,10 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   DeviceGuard g(c->device);
   const int M = cfg->ways;
   if (M < c->K || M > c->n) return fail(MOE_ERR_INVALID_ARG, "ways must satisfy K <= M <= n");
-  if (cfg->miss_mode != MOE_MISS_FETCH && cfg->miss_mode != MOE_MISS_HOST_COMPUTE)
+  if (cfg->miss_mode != MOE_MISS_FETCH && cfg->miss_mode != MOE_MISS_HOST_COMPUTE && cfg->miss_mode != MOE_MISS_PULL)
     return fail(MOE_ERR_INVALID_ARG, "unknown miss_mode");
+  if (cfg->miss_mode == MOE_MISS_PULL && !c->hblob_ok)
+    return fail(MOE_ERR_UNSUPPORTED, "MOE_MISS_PULL needs device-accessible pinned expert blobs");
   if (cfg->miss_mode == MOE_MISS_HOST_COMPUTE && !c->fused)
     return fail(MOE_ERR_UNSUPPORTED, "MOE_MISS_HOST_COMPUTE needs the fused expert kernel (K <= 2)");
   if (cfg->policy != MOE_POLICY_LRU && cfg->policy != MOE_POLICY_FIFO && cfg->policy != MOE_POLICY_STATIC_RANDOM)
@@ -840,6 +873,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.seq = seq;
   ra.sts = c->d_sts ? c->d_sts + (seq % kStsRing) * (kStsHead + 2 * c->fused_grid) : nullptr;
   ra.slot_bytes = c->slot_bytes;
+  ra.hblob = c->d_hblob + (size_t)layer * c->n;
+  ra.last_seq = c->d_last;
 
   ExpertArgs ea;
   ea.route = c->d_route;
@@ -905,6 +940,20 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     CUDA_TRY(launch_route_probe(ra, s, c->pdl));
     prof_end(c, s, &pe);
     c->issued.store(seq, std::memory_order_release);
+    if (c->miss_mode == MOE_MISS_PULL) {  // missed experts: host store -> slots, by the SMs
+      PullJob j;
+      j.count = &c->d_route->K;
+      j.expert = c->d_route->expert;
+      j.slot = c->d_route->slot;
+      j.gen = c->d_route->gen;
+      j.flag = c->d_route->wait;
+      j.hblob = ra.hblob;
+      j.pool = c->pool;
+      j.slot_bytes = c->slot_bytes;
+      j.ready = c->d_ready;
+      j.done = c->d_pull_done;
+      CUDA_TRY(launch_pull(j, c->num_sms, s));
+    }
     prof_begin(c, 1, s, &pe);
     launch_expert_gateup(ea, s, c->num_sms);
     prof_end(c, s, &pe);
@@ -949,10 +998,11 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
   if (!x || !y || T < 1) return fail(MOE_ERR_INVALID_ARG, "bad x / y / T");
   if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(MOE_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
-  if (c->M != c->n || layer >= c->Ncov || c->miss_mode != MOE_MISS_FETCH || c->K > 2 || c->d % 64 ||
+  if (c->M != c->n || layer >= c->Ncov || c->miss_mode == MOE_MISS_HOST_COMPUTE || c->K > 2 || c->d % 64 ||
       c->ffr % 128 || c->policy == MOE_POLICY_STATIC_RANDOM)
     return fail(MOE_ERR_UNSUPPORTED,
-                "prefill needs ways == n, a covered layer, MOE_MISS_FETCH, LRU/FIFO, K <= 2, d % 64 == 0, (ff/P) % 128 == 0");
+                "prefill needs ways == n, a covered layer, MOE_MISS_FETCH or PULL, LRU/FIFO, K <= 2, d % 64 == 0, "
+                "(ff/P) % 128 == 0");
   if (c->P > 1 && !c->comm)
     return fail(MOE_ERR_UNSUPPORTED, "prefill with tp_size > 1 reduces y with NCCL: create the ctx with nccl_unique_id");
   if (c->fetch_error.load()) return fail(MOE_ERR_CUDA, c->fetch_error_msg);
@@ -1000,6 +1050,8 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   // ---- router + cache pass (token order) + plan
   PrefillArgs pa;
   pa.T = T; pa.n = c->n; pa.K = c->K; pa.M = c->M; pa.layer = layer; pa.policy = c->policy;
+  pa.miss_mode = c->miss_mode;
+  pa.last_seq = c->d_last;
   pa.scratch = c->d_pfscratch;
   pa.tag = c->d_tag + (size_t)layer * c->M;
   pa.stamp = c->d_stamp + (size_t)layer * c->M;
@@ -1022,9 +1074,23 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   prof_begin(c, 0, s, &pe);
   CUDA_TRY(launch_prefill_route(pa, c->d_gate + (size_t)layer * c->n * c->d, (const uint16_t*)x, c->d, s));
   prof_end(c, s, &pe);
-  c->issued.store(seq, std::memory_order_release);
+  c->issued.store(seq, std::memory_order_release);  // (the plan kernel publishes seq)
   c->tokens[layer] += (uint32_t)T;
   c->trace_count += (long long)T * c->K;
+  if (c->miss_mode == MOE_MISS_PULL) {  // first-touch experts: host store -> slots, by the SMs
+    PullJob j;
+    j.count = &c->d_plan->nblk;
+    j.expert = c->d_plan->expert;
+    j.slot = c->d_plan->slot;
+    j.gen = c->d_plan->gen;
+    j.flag = c->d_plan->wait;
+    j.hblob = c->d_hblob + (size_t)layer * c->n;
+    j.pool = c->pool;
+    j.slot_bytes = c->slot_bytes;
+    j.ready = c->d_ready;
+    j.done = c->d_pull_done;
+    CUDA_TRY(launch_pull(j, c->num_sms, s));
+  }
   CUDA_TRY(launch_prefill_gather((const uint16_t*)x, c->d, c->d_plan, c->d_xg, rows_cap, s));
   // ---- tensor-core expert FFN: GEMM1 (SwiGLU) then GEMM2 (down + combine)
   const int max_mtiles = rows_cap / 128;
@@ -1032,6 +1098,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   TcArgs ta;
   memset(&ta, 0, sizeof(ta));
   ta.d = c->d; ta.ffr = c->ffr; ta.ldh = c->ffr;
+  ta.num_sms = c->num_sms;
   ta.plan = c->d_plan;
   ta.ready = c->d_ready;
   ta.mode = TC_MODE_SWIGLU;
@@ -1056,7 +1123,6 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
     prof_end(c, s, &pe);
     if (r != ncclSuccess) return fail(MOE_ERR_NCCL, "ncclAllReduce failed");
   }
-  CUDA_TRY(launch_publish_seq(c->d_last, seq, s));
   CUDA_TRY(cudaEventRecord(c->done_ev, s));
   c->any_call = true;
   return MOE_OK;

@@ -389,13 +389,13 @@ def test_host_compute_mixtral_layer_post_fetch_and_hit_under_fill():
         assert st["host_computed"] == st["expert_misses"] and st["fetches"] == st["expert_misses"]
 
 
-def _prefill_run(hm, x, M, warm, policy=moe.POLICY_LRU):
+def _prefill_run(hm, x, M, warm, policy=moe.POLICY_LRU, miss_mode=moe.MISS_FETCH):
     import torch
     T, L, d = x.shape
     dev = torch.device("cuda", 0)
     y = torch.empty((L, T, d), dtype=torch.float32, device=dev)
     with harness.open_moe(hm) as m:
-        m.configure(ways=M, indexes=L, warm_start=warm, policy=policy)
+        m.configure(ways=M, indexes=L, warm_start=warm, policy=policy, miss_mode=miss_mode)
         for l in range(L):   # layer by layer: the whole prompt of layer l in one call
             xl = torch.from_numpy(np.ascontiguousarray(x[:, l, :]).view(np.int16)).to(dev)
             m.prefill(l, xl.data_ptr(), y[l].data_ptr(), T)

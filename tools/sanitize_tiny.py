@@ -5,7 +5,8 @@ c = inputs.CONFIGS["tiny"]
 hm = harness.host_model(c["L"], c["d"], c["ff"], c["n"], c["K"])
 x, _ = harness.hidden_states(hm, 6, "paper")
 ref = oracle.decode(x, hm.gates, lambda l, e: inputs.expert_weights(l, e, hm.d, hm.ff), N=3, M=2, K=2)
-for mode in (moe.MISS_FETCH, moe.MISS_HOST_COMPUTE):
+modes = [int(a) for a in sys.argv[1].split(',')] if len(sys.argv) > 1 else [moe.MISS_FETCH, moe.MISS_HOST_COMPUTE, moe.MISS_PULL]
+for mode in modes:
     with harness.open_moe(hm) as m:
         m.configure(ways=2, indexes=3, miss_mode=mode, host_threads=2)
         y = harness.run_decode(m, x)
@@ -13,6 +14,9 @@ for mode in (moe.MISS_FETCH, moe.MISS_HOST_COMPUTE):
     ok = all(np.array_equal(tr[f].astype(int), ref.records[f].astype(int)) for f in ("expert", "hit", "way", "evicted"))
     err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()) for t in range(6) for l in range(4))
     print("mode", mode, "bitexact", ok, "err", err, flush=True)
+    if err > 1e-4:
+        for t in range(6):
+            print("   t", t, [round(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max()), 6) for l in range(4)])
 # all-hit fast publish path: every expert resident (M = n, warm)
 ref = oracle.decode(x, hm.gates, lambda l, e: inputs.expert_weights(l, e, hm.d, hm.ff), N=4, M=8, K=2, warm_start=True)
 with harness.open_moe(hm) as m:
