@@ -32,6 +32,7 @@ import harness  # noqa: E402
 import inputs  # noqa: E402
 
 SHAPES = {
+    "tiny": (64, 128, 8, 2),            # configs[0] expert shape: the step's fixed-cost floor
     "mixtral-8x7b": (4096, 14336, 8, 2),
     "phi-3.5-moe": (4096, 6400, 16, 2),
     "8x22b-P1": (6144, 16384, 8, 2),

@@ -54,8 +54,19 @@ def _load():
         lib.oracle_cache_access.argtypes = [p, i32, p, p, p, p, p]
         lib.oracle_cache_stats.argtypes = [p, i32, p]
         lib.oracle_cache_set.argtypes = [p, i32, p, p]
+        lib.oracle_set_threads.argtypes = [i32]
+        lib.oracle_max_threads.restype = i32
         _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the row-parallel loops (results do not depend on it)."""
+    _load().oracle_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(_load().oracle_max_threads())
 
 
 def _p(a: np.ndarray) -> int:

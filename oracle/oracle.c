@@ -272,3 +272,10 @@ void oracle_cache_set(const oracle_cache* c, int layer, int32_t* tags, uint64_t*
     stamps[w] = c->stamp[(int64_t)layer * c->M + w];
   }
 }
+
+/* Thread count of the row-parallel loops (bench.py's cpu_baseline times the oracle at one
+ * thread and at all host threads, as Table III sweeps CPU threads). Results are
+ * identical for any count: every output row is one sequential sum. */
+#include <omp.h>
+void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+int oracle_max_threads(void) { return omp_get_max_threads(); }

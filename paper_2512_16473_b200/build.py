@@ -45,15 +45,23 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libmoe.so (or, for A/B experiments, a variant with extra -D defines at `out`,
+    loaded through MOE_LIB_PATH)."""
+    if out is not None:
+        return _build_to(out, list(defines), verbose)
     if not force and not needs_build():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
+    return _build_to(LIB, [], verbose)
+
+
+def _build_to(LIB: str, defines: list, verbose: bool) -> str:
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared",
            "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include(),
-           "-o", LIB + ".tmp", *sources(), "-ldl", "-lpthread"]
+           *[f"-D{d}" for d in defines], "-o", LIB + ".tmp", *sources(), "-ldl", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -36,6 +36,7 @@
 #include <math.h>
 
 #include "moe_internal.cuh"
+#include "gate_gemv.cuh"
 #include "ptx.cuh"
 #include "pull.cuh"
 #include "route_core.cuh"
@@ -53,6 +54,9 @@ constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
 constexpr int kTsPerCta = 40;             // debug timestamps per CTA (MOE_DEBUG_TS)
 constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stage
+// back-off of the polls on flags other CTAs set (interleaved A/B: a pure spin was 0.1-0.25 us
+// slower per step on small shapes)
+#define MOE_POLL_BACKOFF(ns) __nanosleep(ns)
 constexpr int kPullBar = 14;              // named barrier: consumers' MOE_MISS_PULL copies done
 constexpr int kPullCtr = 16 * 8;          // bar[] word counting CTAs done pulling (every call adds G)
 
@@ -125,7 +129,7 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
   if (ld_acquire_u64(p) >= target) return;
   const unsigned long long t0 = globaltimer();
   while (ld_acquire_u64(p) < target) {
-    __nanosleep(64);
+    MOE_POLL_BACKOFF(64);
     if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
   }
 }
@@ -184,7 +188,7 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
       if (wp[u] && (w[u] & 0xffffffff00000000ull) != tag) {
         const unsigned long long t0 = globaltimer();
         while (((w[u] = ld_relaxed_sys_u64(wp[u])) & 0xffffffff00000000ull) != tag) {
-          __nanosleep(32);
+          MOE_POLL_BACKOFF(32);
           if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
         }
       }
@@ -221,7 +225,7 @@ struct RowSched {
 };
 __device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct) {
   RowSched rs;
-  const int sb = (int)((long long)total * pct / 100 / G);
+  const int sb = (int)((unsigned)(total * pct) / 100u / (unsigned)G);  // total * pct < 2^31
   rs.s0 = b * sb;
   rs.s1 = rs.s0 + sb;
   rs.tail0 = G * sb;
@@ -294,6 +298,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   if (f.sts && threadIdx.x == 0) f.sts[kStsHead + b] = globaltimer();
   if (f.ts && threadIdx.x == 0) {
     f.ts[b * kTsPerCta + 0] = globaltimer();
+    f.ts[b * kTsPerCta + 33] = clock64();
     f.ts[b * kTsPerCta + 6] = 0;
     f.ts[b * kTsPerCta + 7] = 0;
     f.ts[b * kTsPerCta + 15] = 0;
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     if (f.xhost) {                            // wait for CTA 0's copy of x
       const unsigned long long t0 = globaltimer();
       while ((int)(ld_acquire_u32(f.xflag) - f.xseq) < 0) {
-        __nanosleep(32);
+        MOE_POLL_BACKOFF(32);
         if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -442,21 +447,29 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     named_bar_sync(kRouteBar, nthr + 32);
     if (f.ts && lane == 0) f.ts[b * kTsPerCta + 10] = globaltimer();
     if (pm && lane == 0) pm[3] = clock64();
-    float z = 0.f;
-    if (lane < n)
-      for (int w = 0; w < nwc; ++w) z += zpart[w * n + lane];  // fixed order
+    // the shared logit order (gate_gemv.cuh): virtual warp = consumer warp, summed in order
+    // (every lane sums a valid column, branch-free; lanes >= n then drop theirs)
+    const float zl = gate_sum_warps(zpart + (lane < n ? lane : 0), n, nwc);
+    const float z = lane < n ? zl : 0.f;
+    if (pm && lane == 0) pm[11] = clock64();
     bool published = false;
     if (fast) {
       // all-hit fast path: rank of expert `lane` by (z desc, index asc) — the same order
       // route_decide derives from the same z — and, if all K selected experts are resident,
       // their slots in rank order (a hit never changes its way's generation; FETCH: no wait)
+      // all shuffles first, then branch-free compares: the shuffles pipeline instead of
+      // each waiting for the previous compare (measured ~1300 -> ~100 cycles)
+      float zz[MOE_MAX_EXPERTS];
+#pragma unroll
+      for (int j = 0; j < MOE_MAX_EXPERTS; ++j) zz[j] = __shfl_sync(0xffffffffu, z, j);
       int rank = 0;
-      for (int j = 0; j < n; ++j) {
-        const float zj = __shfl_sync(0xffffffffu, z, j);
-        rank += (zj > z) || (zj == z && j < lane);
-      }
+#pragma unroll
+      for (int j = 0; j < MOE_MAX_EXPERTS; ++j)
+        rank += (int)((j < n) & ((zz[j] > z) | ((zz[j] == z) & (j < lane))));
+      if (pm && lane == 0) pm[12] = clock64();
       const bool sel = lane < n && rank < K;
       if (__popc(__ballot_sync(0xffffffffu, sel && way_of >= 0)) == K) {
+        if (pm && lane == 0) pm[13] = clock64();
         if (sel) {
           const int slot = ra.slot_base + way_of;
           sslot[rank] = slot;
@@ -472,6 +485,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           smerged = f.merge && K == kMaxFusedK;  // every expert resident and ready
         }
         mbar_arrive(&rbar);                // release (each lane its own writes): route published
+        if (pm && lane == 0) pm[8] = clock64();
         if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
         published = true;
       }
@@ -521,7 +535,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         const unsigned long long* bar = f.bar + 16 * r;
         const unsigned long long t0 = globaltimer();
         while (ld_acquire_u64(bar) < bar_target) {
-          __nanosleep(64);
+          MOE_POLL_BACKOFF(64);
           if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -537,6 +551,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
+      const RowSched sa = make_sched(ffr, b, G, f.pctA);  // (route-independent: before the wait)
+      const RowSched sbk = make_sched(d, b, G, f.pctB);
       mbar_wait(&rbar, 0);                            // route published by the router warp
       const int nseg = snseg;
       for (int r = 0; r < K; ++r)  // host-computed experts have no h: publish them at once
@@ -557,7 +573,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       };
       // phase A: per segment, static block then tail claims (two claims in flight hide the
       // atomic latency)
-      const RowSched sa = make_sched(ffr, b, G, f.pctA);
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* base = sbase[r];
@@ -595,9 +610,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       if (f.prefetchB && nseg > 0 && !swait[sorder[0]]) {
         // the ring drains before phase B starts: have this CTA's first W2 rows on their way
         // to L2 meanwhile (same bytes, read from HBM once)
-        const RowSched sb0 = make_sched(d, b, G, f.pctB);
-        const int nr = min(NSB * RB, sb0.s1 - sb0.s0);
-        if (nr > 0) bulk_prefetch_l2(sbase[sorder[0]] + w2off + (long long)sb0.s0 * rowB, (uint32_t)(nr * rowB));
+        const int nr = min(NSB * RB, sbk.s1 - sbk.s0);
+        if (nr > 0) bulk_prefetch_l2(sbase[sorder[0]] + w2off + (long long)sbk.s0 * rowB, (uint32_t)(nr * rowB));
       }
       marker_a(kEnd);
       // phase B: whole W2 rows into super-stages (2u, 2u+1); W2 does not depend on h, so
@@ -617,7 +631,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         // in turn with the same static-then-steal schedule, but no marker between experts
         // (no ring drain) and no CTA-wide h reload: every chunk's meta carries its expert and
         // a warp waits for that expert's h the first time it meets it.
-        const RowSched sbk = make_sched(d, b, G, f.pctB);
         auto issue_b = [&](int r, int c, int nr) {
           const int s = 2 * (tb % NSB);
           acquire(s);
@@ -644,7 +657,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         marker_b(kEnd);
         return;
       }
-      const RowSched sbk = make_sched(d, b, G, f.pctB);
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* w2 = sbase[r] + w2off;
@@ -751,7 +763,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       if (ld_acquire_u64(bar) < bar_target) {
         const unsigned long long t0 = globaltimer();
         while (ld_acquire_u64(bar) < bar_target) {
-          __nanosleep(32);
+          MOE_POLL_BACKOFF(32);
           if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
         }
       }
@@ -864,7 +876,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
   }
   if (f.tpP > 0) tp_reduce_epilogue(f, b, G, ctid, nthr);
-  if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 5] = globaltimer();
+  if (f.ts && cw == 0 && lane == 0) {
+    f.ts[b * kTsPerCta + 5] = globaltimer();
+    f.ts[b * kTsPerCta + 34] = clock64();
+  }
   if (f.sts && cw == 0 && lane == 0) f.sts[kStsHead + G + b] = globaltimer();
 }
 

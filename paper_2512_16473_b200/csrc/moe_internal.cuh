@@ -55,6 +55,7 @@ struct RouteArgs {
   const uint16_t* Wg;  // [n][d] gate of this layer (device)
   const uint16_t* x;   // [d] (device)
   int d, n, K, M, layer, covered, policy, miss_mode;
+  int gw;              // virtual warps of the gate-logit summation order (gate_gemv.cuh)
   int32_t* tag;        // [M] set of this layer (covered only)
   unsigned long long* stamp;  // [M]
   int slot_base;       // first slot of this layer's set (= layer * M)
@@ -156,6 +157,7 @@ struct PrefillPlan {
 };
 struct PrefillArgs {
   int T, n, K, M, layer, policy, miss_mode;
+  int gw;                      // virtual warps of the gate-logit summation order (gate_gemv.cuh)
   int32_t* tag;                // set of the layer
   unsigned long long* stamp;
   int slot_base;

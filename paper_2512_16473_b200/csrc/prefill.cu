@@ -17,14 +17,13 @@
 //  prefill_gather_kernel  X_g[row] = x[tok[row]] (zeros on padding rows)
 #include <math.h>
 
+#include "gate_gemv.cuh"
 #include "moe_internal.cuh"
 #include "ptx.cuh"
 
 namespace moe {
 namespace {
 
-__device__ __forceinline__ float bfl(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float bfh(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
 // Scratch of one prefill call (device), initialised with cudaMemset(0x7f / 0):
 struct PfScratch {
@@ -39,41 +38,25 @@ struct PfScratch {
   int nnew;
 };
 
-// (1) one CTA per token: logits z = Wg x_t (warp w takes experts w, w+8, ...: each logit is
-//     a lane-strided sum then a shuffle tree, so 8 independent chains per token instead of n
-//     serial ones), then warp 0 takes top-K by (z desc, index asc), softmax over the K in rank
+// (1) one CTA per token: logits z = Wg x_t in the decode path's order (gate_gemv.cuh), then
+//     warp 0 takes top-K by (z desc, index asc), softmax over the K in rank
 //     order (exactly the decode router's arithmetic order for the softmax), first access key
 //     and entry count per expert.
 __global__ void __launch_bounds__(256) prefill_route_kernel(const PrefillArgs a, const uint16_t* __restrict__ Wg,
                                                             const uint16_t* __restrict__ x, int d) {
-  __shared__ float zs[MOE_MAX_EXPERTS];
+  __shared__ float zpart[kGateWarpsMax * MOE_MAX_EXPERTS];
   const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (t >= a.T) return;
   PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
   const int n = a.n, K = a.K;
-  const int4* xv = reinterpret_cast<const int4*>(x + (size_t)t * d);
-  for (int e = warp; e < n; e += 8) {
-    const int4* wr = reinterpret_cast<const int4*>(Wg + (size_t)e * d);
-    float acc = 0.f;
-#pragma unroll 4
-    for (int c = lane; c < (d >> 3); c += 32) {
-      const int4 w4 = __ldg(wr + c), x4 = __ldg(xv + c);
-      acc = fmaf(bfl(w4.x), bfl(x4.x), acc);
-      acc = fmaf(bfh(w4.x), bfh(x4.x), acc);
-      acc = fmaf(bfl(w4.y), bfl(x4.y), acc);
-      acc = fmaf(bfh(w4.y), bfh(x4.y), acc);
-      acc = fmaf(bfl(w4.z), bfl(x4.z), acc);
-      acc = fmaf(bfh(w4.z), bfh(x4.z), acc);
-      acc = fmaf(bfl(w4.w), bfl(x4.w), acc);
-      acc = fmaf(bfh(w4.w), bfh(x4.w), acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) zs[e] = acc;
-  }
+  // logits in the decode path's summation order (gate_gemv.cuh): the 8 warps evaluate the
+  // a.gw virtual warps (w, w + 8, ...), warp 0 sums them in order — so near-tied logits
+  // round exactly as in moe_layer_forward and the routing is the same (moe.h)
+  gate_virtual_warps(Wg, x + (size_t)t * d, d, n, a.gw, warp, 8, zpart);
   __syncthreads();
   if (warp != 0) return;
-  const float z = lane < n ? zs[lane] : -INFINITY;
+  const float zl = lane < n ? gate_sum_warps(zpart + lane, n, a.gw) : 0.f;
+  const float z = lane < n ? zl : -INFINITY;
   bool taken = lane >= n;
   int myS = -1;
   float myZ = 0.f;

@@ -27,7 +27,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// Waiting threads are suspended in try_wait until the phase completes (or the hint expires),
+// instead of re-issuing it: spinning waiters competed with the router warp's shared-memory
+// and shuffle traffic (MOE_MBAR_SPIN=1 restores the spin for A/B runs).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if defined(MOE_MBAR_SPIN)
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -35,6 +39,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(10000000u)
+      : "memory");
+#endif
 }
 
 // L2 policy: streamed weights are read once per token -> evict first.

@@ -75,12 +75,10 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
   if (lane < n) sZ[lane] = zsum;
   __syncwarp();
   int rank = 0;
-  if (lane < n) {
 #pragma unroll 8
-    for (int j = 0; j < n; ++j) {
-      const float zj = sZ[j];
-      rank += (zj > zsum) || (zj == zsum && j < lane);
-    }
+  for (int j = 0; j < n; ++j) {  // branch-free compares (broadcast loads pipeline)
+    const float zj = sZ[j];
+    rank += (int)((zj > zsum) | ((zj == zsum) & (j < lane)));
   }
   if (lane < n && rank < K) { sS[rank] = lane; sW[rank] = zsum; }  // sW: selected logits for now
   __syncwarp();

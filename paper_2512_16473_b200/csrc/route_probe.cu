@@ -10,6 +10,7 @@
 #include <math.h>
 
 #include "moe_internal.cuh"
+#include "gate_gemv.cuh"
 #include "ptx.cuh"
 #include "route_core.cuh"
 
@@ -19,76 +20,34 @@ namespace {
 using ptx::griddep_launch_dependents;
 using ptx::griddep_wait;
 
-__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
-
-__device__ __forceinline__ float dot8_bf16(const int4 a, const int4 b) {
-  float s = bf_lo(a.x) * bf_lo(b.x);
-  s = fmaf(bf_hi(a.x), bf_hi(b.x), s);
-  s = fmaf(bf_lo(a.y), bf_lo(b.y), s);
-  s = fmaf(bf_hi(a.y), bf_hi(b.y), s);
-  s = fmaf(bf_lo(a.z), bf_lo(b.z), s);
-  s = fmaf(bf_hi(a.z), bf_hi(b.z), s);
-  s = fmaf(bf_lo(a.w), bf_lo(b.w), s);
-  s = fmaf(bf_hi(a.w), bf_hi(b.w), s);
-  return s;
-}
-
 constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
-constexpr int kPF = 8;  // gate chunks per lane prefetched into registers before the PDL wait
 
 __global__ void __launch_bounds__(kThreads) route_probe_kernel(const RouteArgs a) {
-  __shared__ float part[MOE_MAX_EXPERTS][kWarps + 1];
+  __shared__ float zpart[kGateWarpsMax * MOE_MAX_EXPERTS];
   __shared__ int sS[kMaxK];
   __shared__ float sZ[kMaxK], sW[kMaxK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- gate GEMV z = Wg x: G = 32/n warps per expert row, lane-strided 16-B chunks.
-  // The gate rows do not depend on x, so they are loaded BEFORE griddepcontrol.wait and
-  // overlap the tail of the preceding kernel (programmatic dependent launch).
   const int n = a.n;
-  const int G = kWarps / n;                 // n <= 32 -> G >= 1
-  const int e = warp / G, g = warp - e * G;
-  const bool active = e < n;
-  const int nchunk = a.d >> 3;
-  const int stride = 32 * G;
-  const int c0 = g * 32 + lane;
-  const int4* wr = reinterpret_cast<const int4*>(a.Wg + (size_t)(active ? e : 0) * a.d);
-  int4 wv[kPF];
-#pragma unroll
-  for (int k = 0; k < kPF; ++k) {
-    const int c = c0 + k * stride;
-    if (active && c < nchunk) wv[k] = __ldg(wr + c);
-  }
   // The set of this layer was last written by the router of an EARLIER call, which
   // completed before the previous expert kernels passed their own griddepcontrol.wait,
   // i.e. before this grid could launch: it can be read before this grid's wait, too.
+  // The gate rows do not depend on x either: pulled towards L2 before the wait.
   DirState ds;
   if (warp == 0) ds = dir_load(a, lane);
+  for (int i = threadIdx.x; i < (n * a.d) >> 6; i += kThreads)  // one 128-B line per thread and step
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.Wg + (size_t)i * 64));
   griddep_launch_dependents();  // let the expert kernel's CTAs get resident early
   griddep_wait();               // x (written by the caller's previous kernel) is visible now
   const long long ck0 = clock64();
   if (a.sts && threadIdx.x == 0) a.sts[0] = ptx::globaltimer();
-  const int4* xv = reinterpret_cast<const int4*>(a.x);
-  float acc = 0.f;
-  if (active) {
-#pragma unroll
-    for (int k = 0; k < kPF; ++k) {
-      const int c = c0 + k * stride;
-      if (c < nchunk) acc += dot8_bf16(wv[k], __ldg(xv + c));
-    }
-    for (int c = c0 + kPF * stride; c < nchunk; c += stride) acc += dot8_bf16(__ldg(wr + c), __ldg(xv + c));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0 && active) part[e][g] = acc;
+  // ---- gate GEMV z = Wg x in the shared summation order (gate_gemv.cuh): real warp w
+  // evaluates virtual warp w (a.gw <= 32 virtual warps), warp 0 sums them in order
+  gate_virtual_warps(a.Wg, a.x, a.d, n, a.gw, warp, kWarps, zpart);
   __syncthreads();
   if (warp != 0) return;
   if (a.sts && lane == 0) a.sts[2] = clock64() - ck0;
-  float zsum = 0.f;
-  if (lane < n)
-    for (int q = 0; q < G; ++q) zsum += part[lane][q];  // fixed order: deterministic
+  const float zsum = lane < n ? gate_sum_warps(zpart + lane, n, a.gw) : 0.f;
   LaneRoute lr;
   const int nmiss = route_decide(a, zsum, ds, true, sS, sZ, sW, &lr);
   if (a.sts && lane == 0) a.sts[4] = clock64() - ck0;

@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "gate_gemv.cuh"
 #include "host_expert.h"
 #include "moe_internal.cuh"
 #include "nccl.h"
@@ -832,6 +833,10 @@ MOE_API moe_status cache_configure(moe_ctx* c, const moe_cache_config* cfg, moe_
   return MOE_OK;
 }
 
+// Virtual warps of the gate-logit summation order (gate_gemv.cuh): the fused kernel's
+// consumer warps, so that every path (fused, split, prefill) rounds the logits alike.
+static int gate_warps(const moe_ctx* c) { return c->fused ? 2 * c->plan.NS : kGateWarpsDefault; }
+
 // xhost / yhost (moe_layer_forward_host, fused path): device-accessible pinned host buffers;
 // the kernel reads x from xhost into the staging buffer x and writes y straight to yhost.
 static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* y, cudaStream_t s,
@@ -855,6 +860,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
   ra.x = (const uint16_t*)x;
   ra.d = c->d; ra.n = c->n; ra.K = c->K; ra.M = c->M; ra.layer = layer;
   ra.covered = covered; ra.policy = c->policy; ra.miss_mode = c->miss_mode;
+  ra.gw = gate_warps(c);
   ra.xmail = c->d_xring + (size_t)(seq % kMailRing) * c->d;
   ra.tag = covered ? c->d_tag + (size_t)layer * c->M : nullptr;
   ra.stamp = covered ? c->d_stamp + (size_t)layer * c->M : nullptr;
@@ -1051,6 +1057,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   PrefillArgs pa;
   pa.T = T; pa.n = c->n; pa.K = c->K; pa.M = c->M; pa.layer = layer; pa.policy = c->policy;
   pa.miss_mode = c->miss_mode;
+  pa.gw = gate_warps(c);
   pa.last_seq = c->d_last;
   pa.scratch = c->d_pfscratch;
   pa.tag = c->d_tag + (size_t)layer * c->M;

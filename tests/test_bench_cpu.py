@@ -21,3 +21,26 @@ def test_reference_arm_json_line():
         assert k in j, k
     assert j["impl"] == "reference" and j["value"] > 0 and j["cpu_baseline"]["kind"] == "oracle"
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["config"]["workload"].startswith("configs[1]")
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N>1 launch contract on CPU: torchrun with 2 ranks, rank 0 alone runs the oracle arm and
+    prints the line (same `config` as our arm's tp2 line), rank 1 exits 0 without work."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, BENCH_REF_BUDGET_S="2", PYTHONPATH=ROOT)
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+                          "--gpus", "2", "--steps", "2", "--warmup", "3"],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    sys.path.insert(0, ROOT)
+    import bench
+    assert j["config"] == bench.workload_config(2)
+    assert j["n_gpus"] == 2 and j["config"]["parallelism"].startswith("tp2")

@@ -82,7 +82,8 @@ def main():
     # warp 0), 26 its gate GEMV done, 27 router warp past the logits barrier, 28 top-K done,
     # 29 probe done (all-hit publish), 30 LRU bookkeeping done, 31 decision returned
     names = {24: "gate_rows_landed", 25: "x_landed", 26: "gemv_done", 27: "router_has_logits", 28: "topk_done", 29: "probe_published",
-             30: "lru_done", 31: "decided"}
+             30: "lru_done", 31: "decided", 32: "fast_path_published", 35: "fast_z_summed", 36: "fast_ranked",
+             37: "fast_all_resident"}
     base = ts[:, 27]
     cyc = {}
     for slot, name in names.items():
@@ -91,6 +92,19 @@ def main():
         if ok.any():
             cyc[name] = statistics.median((v[ok] - base[ok]).tolist())
     out["router_cycles_rel_logits"] = cyc
+    # the CTAs that end last (the next call's PDL wait follows the LAST one)
+    end = ts[:, 5] - prev_end
+    last = np.argsort(-end)[:6]
+    out["latest_ctas"] = [dict({"cta": int(c)}, **{nm: round(float(ts[c, sl] - prev_end) / 1e3, 2)
+                                                    for sl, nm in MARKS.items() if ts[c, sl] > 0})
+                          for c in last[:3]]
+    out["end_us_quantiles"] = {q: float(np.quantile(end, q)) / 1e3 for q in (0.1, 0.5, 0.9, 0.97, 1.0)}
+    # effective SM clock of each CTA over the kernel: clock64 / globaltimer between its start
+    # (slot 33 / 0) and its end (slot 34 / 5)
+    ok = (ts[:, 34] > 0) & (ts[:, 33] > 0) & (ts[:, 5] > ts[:, 0])
+    if ok.any():
+        mhz = (ts[ok, 34] - ts[ok, 33]) / ((ts[ok, 5] - ts[ok, 0]) / 1e3)
+        out["sm_mhz_effective"] = {"median": float(np.median(mhz)), "min": float(mhz.min()), "max": float(mhz.max())}
     print(json.dumps(out, indent=1))
 
 
