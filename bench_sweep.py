@@ -3,6 +3,7 @@
 
     python bench_sweep.py --config mixtral-8x7b --ways 2,4,6,8 --tokens 64
     python bench_sweep.py --config phi-3.5-moe --ways 4,8 --tokens 64
+    python bench_sweep.py --config mixtral-8x7b --ways 2,4,6 --policy lru,fifo,static --tokens 128   (Fig.6)
 
 All L layers' experts live in a pinned host backing store (90.2 GB Mixtral / 80.5 GB Phi);
 the N = L index x M-way GPU cache starts cold; every miss is fetched over PCIe on the fetch
@@ -37,7 +38,9 @@ def main():
     ap.add_argument("--preset", default="paper")
     ap.add_argument("--check-token", type=int, default=-1, help="token whose y is checked vs the oracle (-1 = last)")
     ap.add_argument("--out", default="")
-    ap.add_argument("--miss-mode", default="fetch", choices=["fetch", "host"],
+    ap.add_argument("--policy", default="lru", help="comma list of lru, fifo, static (P:217-218, P:360)")
+    ap.add_argument("--seed", type=int, default=1, help="static policy: seed of the resident draw")
+    ap.add_argument("--miss-mode", default="fetch", choices=["fetch", "host", "pull"],
                     help="fetch: fill the victim slot then compute on the GPU (B200 design); "
                          "host: host cores compute the miss while it is post-fetched (paper P:199-201)")
     ap.add_argument("--host-threads", type=int, default=0)
@@ -73,13 +76,18 @@ def main():
     refy = oracle.decode(x[tc:tc + 1], hm.gates, experts, N=L, M=c["K"], K=c["K"])
     t_oracle = time.time() - t1
     out = []
-    for M in [int(v) for v in args.ways.split(",")]:
+    import paper_2512_16473_b200 as moe
+    POL = {"lru": (oracle.LRU, moe.POLICY_LRU), "fifo": (oracle.FIFO, moe.POLICY_FIFO),
+           "static": (oracle.STATIC, moe.POLICY_STATIC_RANDOM)}
+    runs = [(p, int(v)) for p in args.policy.split(",") for v in args.ways.split(",")]
+    for pol, M in runs:
+        opol, gpol = POL[pol]
         ref = oracle.decode(x, hm.gates, None, N=L, M=M, K=c["K"], compute=False,   # routing + cache replay
-                            warm_start=args.warm)
+                            warm_start=args.warm, policy=opol, seed=args.seed)
         with harness.open_moe(hm) as m:
-            import paper_2512_16473_b200 as moe
-            mm = moe.MISS_HOST_COMPUTE if args.miss_mode == "host" else moe.MISS_FETCH
-            geo = m.configure(ways=M, indexes=L, miss_mode=mm, host_threads=args.host_threads, warm_start=args.warm)
+            mm = {"host": moe.MISS_HOST_COMPUTE, "pull": moe.MISS_PULL}.get(args.miss_mode, moe.MISS_FETCH)
+            geo = m.configure(ways=M, indexes=L, miss_mode=mm, host_threads=args.host_threads, warm_start=args.warm,
+                              policy=gpol, seed=args.seed)
             s = torch.cuda.Stream(dev)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             for t in range(T):
@@ -98,10 +106,11 @@ def main():
         # timed tokens only (exclude the warm-up token) for the rates
         rec = tr[tr["token"] >= 1]
         hits = rec["hit"].reshape(-1, c["K"]).astype(int)
+        oref = ref.records[ref.records["token"] >= 1]["hit"].reshape(-1, c["K"]).astype(int)
         n_acc = hits.shape[0]
         timed_fetch = int((rec["hit"] == 0).sum())
         line = {
-            "config": args.config, "miss_mode": args.miss_mode, "layers": L, "ways": M, "indexes": L,
+            "config": args.config, "miss_mode": args.miss_mode, "policy": pol, "layers": L, "ways": M, "indexes": L,
             "start": "warm" if args.warm else "cold",
             "geometry": geo,
             "tokens_timed": T - 1, "ms": ms, "tokens_per_s": (T - 1) / (ms * 1e-3),
@@ -113,6 +122,8 @@ def main():
             "miss_bytes_gbs": timed_fetch * hm.slot_bytes / (ms * 1e-3) / 1e9,
             "stats_all_tokens": st, "trace_bit_exact_vs_oracle": bool(exact),
             "stats_equal_oracle": bool(stats_equal), "accesses_timed": n_acc,
+            "oracle_hit_rate": {"expert(s)_hit": float((oref.sum(1) > 0).mean()),
+                                "all_k_hit": float((oref.sum(1) == c["K"]).mean()), "per_expert": float(oref.mean())},
             "build_s": t_build,
         }
         y = yd[tc].cpu().numpy()

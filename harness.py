@@ -51,12 +51,22 @@ class HostModel:
 
 
 def host_model(L: int, d: int, ff: int, n: int, K: int, tp_size: int = 1, tp_rank: int = 0,
-               pinned: bool | None = None) -> HostModel:
+               pinned: bool | None = None, touched=None) -> HostModel:
+    """Host backing store of an (L, d, ff, n, K) model. `touched`: optional set of (layer,
+    expert) pairs a workload will route to (known in advance: the hidden states are built for
+    a generated routing, harness.hidden_states); only those get their seeded weights, every
+    other blob pointer aliases one all-zero blob — a full-depth model then needs host memory
+    for the experts it uses only (a mis-routed call would read zeros and fail the parity
+    checks)."""
     torch = _cuda()
     if pinned is None:
         pinned = torch is not None
     sb = moe.slot_bytes(d, ff, tp_size)
-    total = L * n * sb
+    keys = [(l, e) for l in range(L) for e in range(n)]
+    tset = None if touched is None else set(touched)
+    real = keys if tset is None else [k for k in keys if k in tset]
+    nblob = len(real) + (0 if touched is None else 1)
+    total = nblob * sb
     if pinned and torch is not None:
         buf = moe.PinnedBuffer(total)     # cudaHostAlloc, exact size (torch rounds to 2^k)
         arr = buf.array
@@ -65,13 +75,23 @@ def host_model(L: int, d: int, ff: int, n: int, K: int, tp_size: int = 1, tp_ran
         pinned = False
     hm = HostModel(L, d, ff, n, K, tp_size, tp_rank, pinned=pinned, _keep=buf)
     hm.gates = [inputs.gate_weights(l, n, d) for l in range(L)]
-    for l in range(L):
-        for e in range(n):
-            blob = arr[(l * n + e) * sb:(l * n + e + 1) * sb]
-            hm.blobs.append(blob)
+    where = {k: i for i, k in enumerate(real)}
+    if touched is not None:
+        arr[len(real) * sb:(len(real) + 1) * sb] = 0
+    for (l, e) in keys:
+        i = where.get((l, e), len(real))
+        blob = arr[i * sb:(i + 1) * sb]
+        hm.blobs.append(blob)
+        if (l, e) in where:
             w1, w3, w2 = moe.blob_views(blob, d, ff // tp_size)
             inputs.expert_weights_into(w1, w3, w2, l, e, d, ff, tp_rank, tp_size)
     return hm
+
+
+def routed_experts(trace) -> set:
+    """(layer, expert) pairs of a routing trace [T][L][K] (inputs.generate_trace)."""
+    T, L, K = trace.shape
+    return {(l, int(trace[t, l, r])) for t in range(T) for l in range(L) for r in range(K)}
 
 
 def open_moe(hm: HostModel, device: int = 0, nccl_id: bytes | None = None) -> moe.Moe:

@@ -24,6 +24,7 @@
 #include "host_expert.h"
 #include "moe_internal.cuh"
 #include "nccl.h"
+#include "nvtx3/nvToolsExt.h"  // header-only NVTX: ranges for nsys / ncu when a tool is attached
 
 using namespace moe;
 
@@ -114,6 +115,18 @@ struct ProfEv {
   cudaEvent_t a, b;
 };
 
+// Stream timeline (MOE_STREAM_TIMELINE=1, diagnostics): device-timed intervals of every
+// kernel launch on the caller's stream, every weight copy on the fetch stream (P:226's weight
+// channel) and every host-result copy on the activation stream, so the overlap of PCIe
+// transfers with compute can be read without a system profiler (tools/stream_timeline.py).
+enum { TL_KERNEL = 0, TL_FETCH = 1, TL_ACT = 2 };
+struct TlRec {
+  int kind;
+  unsigned long long seq;
+  long long bytes;
+  cudaEvent_t a, b;
+};
+
 struct moe_ctx {
   // shape
   int L = 0, d = 0, ff = 0, n = 0, K = 0, P = 1, rank = 0, ffr = 0, device = 0;
@@ -172,6 +185,10 @@ struct moe_ctx {
   uint64_t prof_launches[MOE_PROF_KINDS] = {0, 0, 0, 0};
   cudaEvent_t done_ev = nullptr;
   cudaEvent_t host_ev = nullptr;  // completion of moe_layer_forward_host
+  bool tl = false;                // MOE_STREAM_TIMELINE
+  std::mutex tl_mu;
+  std::vector<TlRec> tl_recs;
+  cudaEvent_t tl_base = nullptr;
   bool any_call = false;
   // TP
   ncclComm_t comm = nullptr;
@@ -231,6 +248,30 @@ struct DeviceGuard {
   }
 };
 
+cudaEvent_t tl_event() {
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// open / close one timeline interval on stream st (no-ops unless MOE_STREAM_TIMELINE)
+void tl_begin(moe_ctx* c, int kind, unsigned long long seq, long long bytes, cudaStream_t st, TlRec* r) {
+  if (!c->tl) return;
+  r->kind = kind;
+  r->seq = seq;
+  r->bytes = bytes;
+  r->a = tl_event();
+  r->b = tl_event();
+  cudaEventRecord(r->a, st);
+}
+
+void tl_end(moe_ctx* c, cudaStream_t st, TlRec* r) {
+  if (!c->tl) return;
+  cudaEventRecord(r->b, st);
+  std::lock_guard<std::mutex> lk(c->tl_mu);
+  if (c->tl_recs.size() < (1u << 20)) c->tl_recs.push_back(*r);
+}
+
 void fetch_thread_main(moe_ctx* c) {
   cudaSetDevice(c->device);
   const char* dly = getenv("MOE_DEBUG_FETCH_DELAY_US");  // fault injection (tests only)
@@ -281,9 +322,14 @@ void fetch_thread_main(moe_ctx* c) {
       const uint32_t gen = m->gen[i];
       if (delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(delay_us));
       if (log) fprintf(stderr, "[moe fetch] seq=%llu layer=%d expert=%d slot=%d gen=%u\n", next, layer, e, slot, gen);
+      nvtxRangePushA("moe fetch (weight copy, fetch stream)");
+      TlRec tr;
+      tl_begin(c, TL_FETCH, next, c->slot_bytes, c->fetch_stream, &tr);
       cudaError_t err = cudaMemcpyAsync(c->pool + (long long)slot * c->slot_bytes,
                                         c->blobs[(size_t)layer * c->n + e], (size_t)c->slot_bytes,
                                         cudaMemcpyHostToDevice, c->fetch_stream);
+      tl_end(c, c->fetch_stream, &tr);
+      nvtxRangePop();
       CUresult cr = CUDA_SUCCESS;
       if (err == cudaSuccess) cr = publish(c->fetch_stream, c->d_ready + slot, gen);
       note(err, cr);
@@ -294,9 +340,14 @@ void fetch_thread_main(moe_ctx* c) {
       for (int i = 0; i < nmiss; ++i) {
         const int rk = m->rank[i];
         float* o = c->h_hout + (size_t)rk * c->d;
+        nvtxRangePushA("moe host expert (host cores)");
         c->host->ffn(c->blobs[(size_t)layer * c->n + m->expert[i]], x, c->d, c->ffr, o);
+        nvtxRangePop();
+        TlRec tr;
+        tl_begin(c, TL_ACT, next, (long long)sizeof(float) * c->d, c->act_stream, &tr);
         cudaError_t err = cudaMemcpyAsync(c->d_hout + (size_t)rk * c->d, o, sizeof(float) * c->d,
                                           cudaMemcpyHostToDevice, c->act_stream);
+        tl_end(c, c->act_stream, &tr);
         CUresult cr = CUDA_SUCCESS;
         if (err == cudaSuccess) cr = publish(c->act_stream, c->d_hflag + rk, (uint32_t)next);
         note(err, cr);
@@ -602,6 +653,11 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       const char* rb = getenv("MOE_ROWS_B");  // W2 rows per phase-B super-stage (<= plan's)
       if (rb && atoi(rb) >= 1 && atoi(rb) < c->plan.RB) c->plan.RB = atoi(rb);
     }
+    if (getenv("MOE_STREAM_TIMELINE")) {
+      c->tl = true;
+      INIT_TRY(cudaEventCreate(&c->tl_base));
+      INIT_TRY(cudaEventRecord(c->tl_base, c->own_stream));
+    }
     if (getenv("MOE_DEBUG_KERNEL")) {  // progress words in host-mapped memory (slow: PCIe atomics)
       INIT_TRY(cudaHostAlloc((void**)&c->h_dbg, 64, cudaHostAllocMapped));
       memset(c->h_dbg, 0, 64);
@@ -660,6 +716,11 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
     cudaEventDestroy(p.b);
   }
   for (auto e : c->ev_free) cudaEventDestroy(e);
+  for (auto& r : c->tl_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  if (c->tl_base) cudaEventDestroy(c->tl_base);
   free_cache(c);
   cudaFree(c->d_gate);
   cudaFree(c->d_hblob);
@@ -929,12 +990,15 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.xflag = c->d_xflag;
     fa.xseq = xhost ? ++c->xseq : 0u;
     prof_begin(c, 1, s, &pe);
+    TlRec tr;
+    tl_begin(c, TL_KERNEL, seq, 0, s, &tr);
     cudaError_t e = launch_expert_fused(fa, c->plan, c->fused_grid, s, c->pdl, c->coop);
     if (e != cudaSuccess && c->pdl) {  // PDL not accepted: retry without it
       cudaGetLastError();
       c->pdl = false;
       e = launch_expert_fused(fa, c->plan, c->fused_grid, s, false, c->coop);
     }
+    tl_end(c, s, &tr);
     prof_end(c, s, &pe);
     if (e != cudaSuccess) return fail(MOE_ERR_CUDA, std::string("expert_fused launch: ") + cudaGetErrorString(e));
     c->fused_calls += 1;
@@ -984,7 +1048,40 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
 MOE_API moe_status moe_layer_forward(moe_ctx* c, int32_t layer, const void* x, float* y, void* stream) {
   if (!c) return fail(MOE_ERR_INVALID_ARG, "NULL ctx");
   DeviceGuard g(c->device);
-  return forward_impl(c, layer, x, y, (cudaStream_t)stream);
+  nvtxRangePushA("moe_layer_forward");
+  const moe_status st = forward_impl(c, layer, x, y, (cudaStream_t)stream);
+  nvtxRangePop();
+  return st;
+}
+
+// Debug only (not in moe.h): the stream timeline recorded since the last read
+// (MOE_STREAM_TIMELINE=1). out: [cap][5] doubles {kind (0 kernel on the caller's stream,
+// 1 weight copy on the fetch stream, 2 host-result copy on the activation stream), call seq,
+// start ms, end ms (relative to the context's base event), bytes}. Synchronizes. Returns the
+// number of records written (and clears them), or -1.
+MOE_API int64_t moe_debug_stream_timeline(moe_ctx* c, double* out, int64_t cap) {
+  if (!c || !c->tl || (cap > 0 && !out)) return -1;
+  DeviceGuard g(c->device);
+  if (drain(c) != MOE_OK) return -1;
+  std::lock_guard<std::mutex> lk(c->tl_mu);
+  int64_t n = 0;
+  for (auto& r : c->tl_recs) {
+    float t0 = 0.f, t1 = 0.f;
+    if (n < cap && cudaEventElapsedTime(&t0, c->tl_base, r.a) == cudaSuccess &&
+        cudaEventElapsedTime(&t1, c->tl_base, r.b) == cudaSuccess) {
+      out[5 * n + 0] = r.kind;
+      out[5 * n + 1] = (double)r.seq;
+      out[5 * n + 2] = t0;
+      out[5 * n + 3] = t1;
+      out[5 * n + 4] = (double)r.bytes;
+      ++n;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  cudaGetLastError();
+  c->tl_recs.clear();
+  return n;
 }
 
 // m-tiles per CTA tile of the prefill GEMMs: 0 = chosen on the device from the exact tile
