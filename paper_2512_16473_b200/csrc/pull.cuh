@@ -32,7 +32,10 @@ __device__ __forceinline__ void pull_share(long long bytes, int b, int G, long l
 // dst[i] = src[i] for 16-B units i in [u0, u1), threads tid = 0 .. nthr-1 of the caller.
 __device__ __forceinline__ void pull_copy(uint8_t* dst, const uint8_t* src, long long u0, long long u1, int tid,
                                           int nthr) {
-  constexpr int U = 4;  // independent loads in flight per thread
+#ifndef MOE_PULL_U
+#define MOE_PULL_U 4
+#endif
+  constexpr int U = MOE_PULL_U;  // independent loads in flight per thread
   const int4* s = reinterpret_cast<const int4*>(src);
   int4* d = reinterpret_cast<int4*>(dst);
   for (long long i = u0 + tid; i < u1; i += (long long)U * nthr) {
