@@ -303,6 +303,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     f.ts[b * kTsPerCta + 7] = 0;
     f.ts[b * kTsPerCta + 15] = 0;
     f.ts[b * kTsPerCta + 16] = 0;
+    f.ts[b * kTsPerCta + 19] = 0;
+    f.ts[b * kTsPerCta + 20] = 0;
+    f.ts[b * kTsPerCta + 22] = 0;
+    f.ts[b * kTsPerCta + 23] = 0;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -538,6 +542,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           MOE_POLL_BACKOFF(64);
           if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
         }
+        if (f.ts) f.ts[b * kTsPerCta + 19 + si] = globaltimer();  // h of segment si published grid-wide
         asm volatile("fence.proxy.async.global;" ::: "memory");
         mbar_arrive_expect_tx(hbarK + r, (uint32_t)ffr * 4u);
         bulk_g2s(xh + f.hoff + (size_t)r * f.hstride, a.h + (long long)r * ffr, (uint32_t)ffr * 4u, hbarK + r,
@@ -817,6 +822,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         if (mm && !((seen >> r) & 1u)) {   // merged: h_r copied in by the router warp
           mbar_wait(hbarK + r, 0);
           seen |= 1u << r;
+          if (f.ts && cw == 0 && lane == 0 && r == sorder[1 % nseg]) f.ts[b * kTsPerCta + 22] = globaltimer();
         }
         // h_r[8k .. 8k+3] / h_r[8k+4 .. 8k+7] (2-plane layout)
         const float4* hp0 = reinterpret_cast<const float4*>(xh + (mm ? f.hoff + (size_t)r * f.hstride : 0));
@@ -834,6 +840,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           if (lane == 0) pb[4 * i + q] = sum;
         }
         named_bar_sync(bid, 128);          // the 4 quarters of these rows are done
+        if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 23] = globaltimer();  // (last: final B chunk)
         if (q == 0) {                      // lane i combines row i in a fixed order
           float o = 0.f;
           if (lane < nr) o = ((pb[4 * lane] + pb[4 * lane + 1]) + pb[4 * lane + 2]) + pb[4 * lane + 3];

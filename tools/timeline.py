@@ -32,7 +32,9 @@ import paper_2512_16473_b200 as moe  # noqa: E402
 MARKS = {0: "cta_start", 8: "pdl_wait_done", 9: "x_landed", 10: "router_has_logits", 1: "route_published",
          11: "route_decided", 2: "first_row_consumed", 3: "phase_A_done", 4: "phase_B_first_h", 6: "phase_B_second_h",
          5: "cta_end", 12: "prod_last_A_issued", 13: "prod_last_Bo0_issued", 14: "prod_last_B_issued",
-         15: "first_B_row_seen", 16: "cta_out_of_phase_A", 17: "h_first_published"}
+         15: "first_B_row_seen", 16: "cta_out_of_phase_A", 17: "h_first_published",
+         19: "merged_h0_published", 20: "merged_h1_published", 22: "merged_h1_landed_warp0",
+         23: "warp0_last_B_chunk_done"}
 KSTS_RING, KSTS_HEAD = 64, 8
 
 
