@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--tokens", default="128,512,2048,4096")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--check", type=int, default=4, help="tokens checked against the oracle per T")
+    ap.add_argument("--ways", type=int, default=0, help="cache ways M (default n: nothing evicted; M < n: "
+                    "evictions inside the prompt, the cache pass replays the accesses in order)")
     args = ap.parse_args()
     import torch
 
@@ -41,6 +43,7 @@ def main():
     c = inputs.CONFIGS[args.shape]
     d, ff, n, K = c["d"], c["ff"], c["n"], c["K"]
     hm = harness.host_model(1, d, ff, n, K)
+    M = args.ways or n
     dev = torch.device("cuda", 0)
     W = {}
     for T in [int(v) for v in args.tokens.split(",")]:
@@ -48,7 +51,7 @@ def main():
         xd = torch.from_numpy(np.ascontiguousarray(x[:, 0, :]).view(np.int16)).to(dev)
         yd = torch.empty((T, d), dtype=torch.float32, device=dev)
         with harness.open_moe(hm) as m:
-            m.configure(ways=n, indexes=1, warm_start=True)
+            m.configure(ways=M, indexes=1, warm_start=True)
             s = torch.cuda.Stream(dev)
             for _ in range(3):
                 m.prefill(0, xd.data_ptr(), yd.data_ptr(), T, s.cuda_stream)
@@ -86,7 +89,7 @@ def main():
             r = oracle.decode(x[t:t + 1], hm.gates, experts, N=1, M=n, K=K, warm_start=True)
             errs.append(float(np.abs(ybuf[t] - r.y[0, 0]).max() / np.abs(r.y[0, 0]).max()))
         peak = float(peaks["bf16_tflops"])
-        line = {"workload": f"prefill: one {args.shape}-shaped MoE layer (d={d}, ff={ff}, {n} experts top-{K}), M={n} warm",
+        line = {"workload": f"prefill: one {args.shape}-shaped MoE layer (d={d}, ff={ff}, {n} experts top-{K}), M={M} warm",
                 "T": T, "ms": ms, "tokens_per_s": T / (ms * 1e-3), "distinct_experts": distinct,
                 "tflops_total": (flops_g1 + flops_g2) / (ms * 1e-3) / 1e12,
                 "gemm_swiglu": {"ms": g1, "tflops": flops_g1 / (g1 * 1e-3) / 1e12,

@@ -48,6 +48,7 @@ struct Mail {
   uint32_t gen[kMaxK];
   int32_t rank[kMaxK];       // routing rank of the miss
   int32_t postfetch[kMaxK];  // 1: copy the weights into `slot` (covered miss)
+  int32_t dest[kMaxK];       // 0: `slot` of the pool; 1: `slot` of the prefill staging area (M < n)
   int32_t host;              // 1: the host computes these experts (x is in the call's x slot)
 };
 
@@ -152,6 +153,8 @@ struct PrefillPlan {
   uint32_t gen[kPrefillMaxBlk];
   int wait[kPrefillMaxBlk];   // 1: the slot is filled by this call -> wait for gen
   int expert[kPrefillMaxBlk]; // expert of each block
+  int stage[kPrefillMaxBlk];  // 1: `slot` indexes the prefill staging area (M < n: routed in the
+                              //    prompt but not resident at its end), 0: the slot pool
   int* tok;      // [rows_cap] token of each gathered row (-1 = padding)
   float* wrow;   // [rows_cap] gate weight of that token for the block's expert
 };
@@ -175,6 +178,11 @@ struct PrefillArgs {
   long long slot_bytes;
   PrefillPlan* plan;
   void* scratch;               // prefill_scratch_bytes() of device scratch
+  // M < n (evictions inside the prompt): the cache pass replays the T accesses in order
+  float* zbuf;                 // [T][n] router logits
+  const uint32_t* ready;       // landed generation per pool slot
+  int staging_base;            // (RouteArgs field; unused: prefill layers are covered)
+  int stage_slots;             // prefill staging slots (n - M)
 };
 // MOE_MISS_PULL outside the fused kernel (split decode path, prefill): copy the listed
 // blobs (flag[i] != 0, i < *count) from the pinned host store into their slots, then
@@ -186,6 +194,8 @@ struct PullJob {
   const uint32_t* gen;
   const int32_t* flag;
   const uint8_t* const* hblob;  // [n] blobs of the layer
+  const int32_t* only;          // optional: copy entry i only if only[i] == only_val
+  int only_val;
   uint8_t* pool;
   long long slot_bytes;
   uint32_t* ready;
@@ -211,6 +221,9 @@ struct TcArgs {
   float* y;                    // DOWN: y [T][d]
   const PrefillPlan* plan;     // SWIGLU / DOWN
   const uint32_t* ready;       // landed fill generation per slot
+  CUtensorMap mapB2;           // B operand view of the prefill staging area (plan->stage blocks)
+  const uint32_t* ready2;      // landed fill generation per staging slot
+  int has_stage;               // mapB2 / ready2 valid
   int num_sms;                 // persistent grid size (0: the current device's SM count)
   int mt_c2;                   // >0: both m-tiles-per-tile variants are launched and each exits
                                // unless the exact tile counts pick it (cost of a 2-m-tile tile

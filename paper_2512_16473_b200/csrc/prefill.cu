@@ -20,6 +20,7 @@
 #include "gate_gemv.cuh"
 #include "moe_internal.cuh"
 #include "ptx.cuh"
+#include "route_core.cuh"
 
 namespace moe {
 namespace {
@@ -36,6 +37,10 @@ struct PfScratch {
   int offs[MOE_MAX_EXPERTS];                  // row offset of e's block in X_g
   unsigned long long clock0;
   int nnew;
+  // M < n (evictions inside the prompt): the set before and after the replayed accesses
+  int tag0[MOE_MAX_EXPERTS], tag1[MOE_MAX_EXPERTS];
+  uint32_t gen0[MOE_MAX_EXPERTS], gen1[MOE_MAX_EXPERTS];
+  int mn;  // 1: this call takes the M < n path (lists kernel leaves stamps and clock alone)
 };
 
 // (1) one CTA per token: logits z = Wg x_t in the decode path's order (gate_gemv.cuh), then
@@ -56,6 +61,7 @@ __global__ void __launch_bounds__(256) prefill_route_kernel(const PrefillArgs a,
   __syncthreads();
   if (warp != 0) return;
   const float zl = lane < n ? gate_sum_warps(zpart + lane, n, a.gw) : 0.f;
+  if (a.zbuf && lane < n) a.zbuf[(size_t)t * n + lane] = zl;  // M < n: replayed by prefill_seq_kernel
   const float z = lane < n ? zl : -INFINITY;
   bool taken = lane >= n;
   int myS = -1;
@@ -141,6 +147,7 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
       a.mail->gen[nnew] = g;
       a.mail->rank[nnew] = 0;
       a.mail->postfetch[nnew] = 1;
+      a.mail->dest[nnew] = 0;
     }
     ++nnew;
   }
@@ -158,6 +165,7 @@ __global__ void __launch_bounds__(64) prefill_plan_kernel(const PrefillArgs a) {
     a.plan->gen[nb] = gen[way[e]];
     a.plan->wait[nb] = isnew[e];
     a.plan->expert[nb] = e;
+    a.plan->stage[nb] = 0;
     sc->offs[e] = off;
     off += tiles * 128;
     mt += tiles;
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(1024) prefill_lists_kernel(const PrefillArgs a
   __shared__ int part[1024];
   const PfScratch* sc = reinterpret_cast<const PfScratch*>(a.scratch);
   const int e = blockIdx.x, K = a.K, T = a.T;
-  if (e == 0 && threadIdx.x < a.n) {
+  if (e == 0 && threadIdx.x < a.n && !sc->mn) {
     const int ex = threadIdx.x;
     if (sc->cnt[ex] > 0) {
       if (a.policy == MOE_POLICY_LRU) a.stamp[sc->way[ex]] = sc->lastc[ex];
@@ -296,6 +304,120 @@ __global__ void __launch_bounds__(1024) prefill_lists_kernel(const PrefillArgs a
   }
 }
 
+// ---- M < n: the prompt's accesses can evict, so the cache pass is the decode router's own
+// decision (route_core.cuh) replayed token by token by one warp, with the set's state kept in
+// registers between tokens: routing (from the batched router's logits, the shared summation
+// order), hit/miss, LRU/FIFO update, victims, trace records and counters are those of T
+// successive moe_layer_forward calls by construction. The expert FFN then runs batched per
+// distinct routed expert: experts resident at the end of the prompt are read from their
+// (re)filled slots, the others from the prefill staging area (prefill_plan_mn_kernel).
+__global__ void __launch_bounds__(32) prefill_seq_kernel(const PrefillArgs a) {
+  __shared__ int sS[kMaxK];
+  __shared__ float sZ[MOE_MAX_EXPERTS], sW[kMaxK];
+  PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
+  const int lane = threadIdx.x;
+  RouteArgs ra;
+  memset(&ra, 0, sizeof(ra));
+  ra.d = 0; ra.n = a.n; ra.K = a.K; ra.M = a.M; ra.layer = a.layer; ra.covered = 1; ra.policy = a.policy;
+  ra.miss_mode = MOE_MISS_PULL;  // (no mailbox entries: the plan below decides the physical fills)
+  ra.tag = a.tag; ra.stamp = a.stamp; ra.slot_base = a.slot_base; ra.staging_base = a.staging_base;
+  ra.gen = a.gen; ra.ready = a.ready; ra.clock = a.clock; ra.stats = a.stats; ra.trace = a.trace;
+  ra.trace_cap = a.trace_cap; ra.slot_bytes = a.slot_bytes;
+  DirState ds = dir_load(ra, lane);
+  if (lane < a.M) {
+    sc->tag0[lane] = ds.tag;
+    sc->gen0[lane] = ds.gen;
+  }
+  if (lane == 0) {
+    sc->mn = 1;
+    sc->clock0 = ds.clock;
+  }
+  float znext = lane < a.n ? a.zbuf[lane] : 0.f;
+  for (int t = 0; t < a.T; ++t) {
+    const float z = znext;
+    if (t + 1 < a.T && lane < a.n) znext = a.zbuf[(size_t)(t + 1) * a.n + lane];  // next token's logits in flight
+    ra.token = a.token0 + (uint32_t)t;
+    ra.trace_idx = a.trace_idx + (long long)t * a.K;
+    LaneRoute lr;
+    DirState nx;
+    route_decide(ra, z, ds, true, sS, sZ, sW, &lr, nullptr, NoEarlyRoute(), &nx);
+    ds.tag = nx.tag;
+    ds.stamp = nx.stamp;
+    ds.gen = nx.gen;
+    ds.clock = nx.clock;
+  }
+  if (lane < a.M) {
+    sc->tag1[lane] = ds.tag;
+    sc->gen1[lane] = ds.gen;
+  }
+}
+
+// M < n: plan blocks (expert id order) and the physical fills. A routed expert resident at
+// the end of the prompt in way v is read from slot v; it needs a fill unless it already sat in
+// v before the prompt with no insertion into v since (same generation). Every other routed
+// expert gets a prefill staging slot and a fill (staging generation = the call's seq).
+__global__ void __launch_bounds__(32) prefill_plan_mn_kernel(const PrefillArgs a) {
+  PfScratch* sc = reinterpret_cast<PfScratch*>(a.scratch);
+  if (threadIdx.x != 0) return;
+  const int n = a.n, M = a.M;
+  const bool mailbox = a.miss_mode != MOE_MISS_PULL;
+  int nb = 0, off = 0, mt = 0, nfill = 0, nst = 0;
+  for (int e = 0; e < n; ++e) {
+    const int cnt = sc->cnt[e];
+    if (!cnt) continue;
+    int v = -1;
+    for (int w = 0; w < M; ++w)
+      if (sc->tag1[w] == e) v = w;
+    int slot, stage, fill;
+    uint32_t g;
+    if (v >= 0) {
+      slot = a.slot_base + v;
+      stage = 0;
+      g = sc->gen1[v];
+      fill = !(sc->tag0[v] == e && sc->gen0[v] == g);
+    } else {
+      slot = nst++;
+      stage = 1;
+      g = (uint32_t)a.seq;
+      fill = 1;
+    }
+    const int tiles = (cnt + 127) / 128;
+    a.plan->row_off[nb] = off;
+    a.plan->mt_pref[nb] = mt;
+    a.plan->slot[nb] = slot;
+    a.plan->gen[nb] = g;
+    a.plan->wait[nb] = fill;
+    a.plan->expert[nb] = e;
+    a.plan->stage[nb] = stage;
+    sc->offs[e] = off;
+    off += tiles * 128;
+    mt += tiles;
+    ++nb;
+    if (fill && mailbox) {
+      a.mail->expert[nfill] = e;
+      a.mail->slot[nfill] = slot;
+      a.mail->gen[nfill] = g;
+      a.mail->rank[nfill] = 0;
+      a.mail->postfetch[nfill] = 1;
+      a.mail->dest[nfill] = stage;
+    }
+    nfill += fill;
+  }
+  a.plan->mt_pref[nb] = mt;
+  a.plan->nblk = nb;
+  a.plan->total_mtiles = mt;
+  a.plan->rows = off;
+  if (nfill && mailbox) {
+    a.mail->layer = a.layer;
+    a.mail->nmiss = nfill;
+    a.mail->host = 0;
+    __threadfence_system();
+    a.mail->seq = a.seq;
+    __threadfence_system();
+  }
+  *a.last_seq = a.seq;
+}
+
 __global__ void __launch_bounds__(256) prefill_gather_kernel(const uint16_t* __restrict__ x, int d,
                                                              const PrefillPlan* __restrict__ plan,
                                                              uint16_t* __restrict__ xg, int rows_cap) {
@@ -324,6 +446,8 @@ cudaError_t preload_prefill_kernels() {
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_lists_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_gather_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, publish_seq_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_seq_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, prefill_plan_mn_kernel);
   return e;
 }
 
@@ -337,8 +461,13 @@ cudaError_t launch_prefill_route(const PrefillArgs& a, const uint16_t* Wg, const
   if (e != cudaSuccess) return e;
   const int blocks = (a.T + 7) / 8;
   prefill_route_kernel<<<a.T, 256, 0, s>>>(a, Wg, x, d);
-  prefill_plan_kernel<<<1, 64, 0, s>>>(a);
-  prefill_access_kernel<<<blocks, 256, 0, s>>>(a);
+  if (a.M < a.n) {  // evictions inside the prompt: replay the accesses in order
+    prefill_seq_kernel<<<1, 32, 0, s>>>(a);
+    prefill_plan_mn_kernel<<<1, 32, 0, s>>>(a);
+  } else {
+    prefill_plan_kernel<<<1, 64, 0, s>>>(a);
+    prefill_access_kernel<<<blocks, 256, 0, s>>>(a);
+  }
   prefill_lists_kernel<<<a.n, 1024, 0, s>>>(a);
   return cudaGetLastError();
 }

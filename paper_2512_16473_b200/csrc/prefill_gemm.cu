@@ -165,11 +165,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
     if (lane == 0) {
       prefetch_tmap(&p.mapA);
       prefetch_tmap(&p.mapB);
+      if (p.has_stage) prefetch_tmap(&p.mapB2);
       int it = 0;  // global k-block counter (ring position)
       for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
         const TileCoord tc = tile_of<MT>(p, BN, id);
-        if (p.mode != TC_MODE_PLAIN && p.plan->wait[tc.blk])  // expert filled by this call
-          ptx::wait_ready(p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
+        // (M < n prefill) a routed expert not resident at the end of the prompt lives in the
+        // staging area: its B operand comes through the staging view
+        const bool stg = p.mode != TC_MODE_PLAIN && p.has_stage && p.plan->stage[tc.blk];
+        const CUtensorMap* mb = stg ? &p.mapB2 : &p.mapB;
+        if (p.mode != TC_MODE_PLAIN && p.plan->wait[tc.blk]) {  // expert filled by this call
+          ptx::wait_ready(stg ? p.ready2 : p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int kb = 0; kb < ktiles; ++kb, ++it) {
           const int s = it % C::kStages;
           ptx::mbar_wait(empty + s, ((it / C::kStages) & 1) ^ 1);
@@ -178,7 +185,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
           // (a short group's extra A tile reads the following rows / TMA zero fill: unused)
           for (int i = 0; i < MT; ++i) tma_load_2d(st + i * C::kA, &p.mapA, kb * BK, tc.a_row + i * BM, full + s);
           for (int j = 0; j < NB; ++j)
-            tma_load_2d(st + MT * C::kA + j * C::kB, &p.mapB, kb * BK, tc.b_row[j], full + s);
+            tma_load_2d(st + MT * C::kA + j * C::kB, mb, kb * BK, tc.b_row[j], full + s);
         }
       }
     }

@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(kPullThreads) pull_kernel(const PullJob j) {
   __shared__ bool last;
   const int cnt = *j.count;
   for (int i = 0; i < cnt; ++i) {
-    if (!j.flag[i]) continue;
+    if (!j.flag[i] || (j.only && j.only[i] != j.only_val)) continue;
     long long u0, u1;
     pull_share(j.slot_bytes, blockIdx.x, gridDim.x, &u0, &u1);
     pull_copy(j.pool + (long long)j.slot[i] * j.slot_bytes, j.hblob[j.expert[i]], u0, u1, threadIdx.x, kPullThreads);
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(kPullThreads) pull_kernel(const PullJob j) {
   if (!last) return;
   __threadfence();
   for (int i = threadIdx.x; i < cnt; i += kPullThreads)
-    if (j.flag[i]) *((volatile uint32_t*)(j.ready + j.slot[i])) = j.gen[i];
+    if (j.flag[i] && (!j.only || j.only[i] == j.only_val)) *((volatile uint32_t*)(j.ready + j.slot[i])) = j.gen[i];
   if (threadIdx.x == 0) *j.done = 0u;
 }
 

@@ -64,10 +64,13 @@ struct NoEarlyRoute {
 // K holding rank r's final slot, generation and wait flag — not yet its gate weight) as
 // soon as the slots are known, before the softmax and the cache bookkeeping: the caller
 // may start streaming then.
+// `next` (optional): the set's state after this access (tag/stamp/gen per way lane, clock),
+// for callers that replay several accesses in a row (moe_layer_prefill with M < n).
 template <class Early = NoEarlyRoute>
 __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum, const DirState& ds,
                                             const bool writer, int* sS, float* sZ, float* sW, LaneRoute* out,
-                                            unsigned long long* dts = nullptr, Early early = Early()) {
+                                            unsigned long long* dts = nullptr, Early early = Early(),
+                                            DirState* next = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n = a.n, K = a.K, M = a.M;
   // ---- top-K by (z desc, index asc): lane e counts the experts that precede it (one
@@ -169,6 +172,13 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
       if (lane == v) { tag = sS[r]; st = clock; ++gen; }
       if (lane == r) { myWay = v; myEv = ev; }
     }
+    if (next) {
+      next->tag = tag;
+      next->stamp = st;
+      next->gen = gen;
+      next->clock = clock;
+      next->sgen = ds.sgen;
+    }
     // write the set back; per-rank slot / generation
     if (writer && lane < M && !is_static) {
       a.tag[lane] = tag;
@@ -258,6 +268,7 @@ __device__ __forceinline__ int route_decide(const RouteArgs& a, const float zsum
       a.mail->gen[i] = myGen;
       a.mail->rank[i] = lane;
       a.mail->postfetch[i] = myPost;
+      a.mail->dest[i] = 0;
     }
   }
   if (lane == 0) {

@@ -226,6 +226,14 @@ struct moe_ctx {
   uint16_t* d_hg = nullptr;
   CUtensorMap map_xg{}, map_hg{}, map_pool_d{}, map_pool_f{};
   bool pool_maps = false;
+  // prefill with M < n: logits of the prompt, staging area for routed experts that are not
+  // resident at the end of the prompt (n - M slots), its landed generations and tensor maps
+  float* d_zbuf = nullptr;
+  int zbuf_T = 0;
+  uint8_t* d_pfstage = nullptr;
+  int pfstage_slots = 0;
+  uint32_t* d_pfready = nullptr;
+  CUtensorMap map_stage_d{}, map_stage_f{};
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
@@ -325,13 +333,14 @@ void fetch_thread_main(moe_ctx* c) {
       nvtxRangePushA("moe fetch (weight copy, fetch stream)");
       TlRec tr;
       tl_begin(c, TL_FETCH, next, c->slot_bytes, c->fetch_stream, &tr);
-      cudaError_t err = cudaMemcpyAsync(c->pool + (long long)slot * c->slot_bytes,
+      const bool stg = m->dest[i] != 0;  // prefill (M < n) staging slot instead of a pool slot
+      cudaError_t err = cudaMemcpyAsync((stg ? c->d_pfstage : c->pool) + (long long)slot * c->slot_bytes,
                                         c->blobs[(size_t)layer * c->n + e], (size_t)c->slot_bytes,
                                         cudaMemcpyHostToDevice, c->fetch_stream);
       tl_end(c, c->fetch_stream, &tr);
       nvtxRangePop();
       CUresult cr = CUDA_SUCCESS;
-      if (err == cudaSuccess) cr = publish(c->fetch_stream, c->d_ready + slot, gen);
+      if (err == cudaSuccess) cr = publish(c->fetch_stream, (stg ? c->d_pfready : c->d_ready) + slot, gen);
       note(err, cr);
     }
     // activation channel: the host cores compute the missed experts
@@ -743,6 +752,9 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_wrow);
   cudaFree(c->d_xg);
   cudaFree(c->d_hg);
+  cudaFree(c->d_zbuf);
+  cudaFree(c->d_pfstage);
+  cudaFree(c->d_pfready);
   if (c->h_xring) cudaFreeHost(c->h_xring);
   if (c->h_hout) cudaFreeHost(c->h_hout);
   if (c->act_stream) cudaStreamDestroy(c->act_stream);
@@ -1011,7 +1023,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     prof_end(c, s, &pe);
     c->issued.store(seq, std::memory_order_release);
     if (c->miss_mode == MOE_MISS_PULL) {  // missed experts: host store -> slots, by the SMs
-      PullJob j;
+      PullJob j{};
       j.count = &c->d_route->K;
       j.expert = c->d_route->expert;
       j.slot = c->d_route->slot;
@@ -1101,10 +1113,10 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
   if (!x || !y || T < 1) return fail(MOE_ERR_INVALID_ARG, "bad x / y / T");
   if (((uintptr_t)x & 15) || ((uintptr_t)y & 15)) return fail(MOE_ERR_INVALID_ARG, "x and y must be 16-byte aligned");
-  if (c->M != c->n || layer >= c->Ncov || c->miss_mode == MOE_MISS_HOST_COMPUTE || c->K > 2 || c->d % 64 ||
-      c->ffr % 128 || c->policy == MOE_POLICY_STATIC_RANDOM)
+  if (layer >= c->Ncov || c->miss_mode == MOE_MISS_HOST_COMPUTE || c->K > 2 || c->d % 64 || c->ffr % 128 ||
+      c->policy == MOE_POLICY_STATIC_RANDOM)
     return fail(MOE_ERR_UNSUPPORTED,
-                "prefill needs ways == n, a covered layer, MOE_MISS_FETCH or PULL, LRU/FIFO, K <= 2, d % 64 == 0, "
+                "prefill needs a covered layer, MOE_MISS_FETCH or PULL, LRU/FIFO, K <= 2, d % 64 == 0, "
                 "(ff/P) % 128 == 0");
   if (c->P > 1 && !c->comm)
     return fail(MOE_ERR_UNSUPPORTED, "prefill with tp_size > 1 reduces y with NCCL: create the ctx with nccl_unique_id");
@@ -1139,6 +1151,36 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
     c->pf_T = T;
     c->pf_rows = rows_cap;
   }
+  const bool mn = c->M < c->n;  // evictions possible inside the prompt
+  if (mn && (T > c->zbuf_T || c->pfstage_slots != c->n - c->M)) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (T > c->zbuf_T) {
+      cudaFree(c->d_zbuf);
+      c->d_zbuf = nullptr;
+      c->zbuf_T = 0;
+      CUDA_TRY(cudaMalloc(&c->d_zbuf, sizeof(float) * (size_t)T * c->n));
+      c->zbuf_T = T;
+    }
+    if (c->pfstage_slots != c->n - c->M) {
+      cudaFree(c->d_pfstage);
+      c->d_pfstage = nullptr;
+      c->pfstage_slots = 0;
+      const int ns = c->n - c->M;
+      cudaError_t e = cudaMalloc(&c->d_pfstage, (size_t)ns * c->slot_bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        c->d_pfstage = nullptr;
+        return fail(MOE_ERR_OUT_OF_MEMORY, "prefill staging area (n - M slots) cudaMalloc failed");
+      }
+      if (!c->d_pfready) CUDA_TRY(cudaMalloc(&c->d_pfready, sizeof(uint32_t) * MOE_MAX_EXPERTS));
+      CUDA_TRY(cudaMemset(c->d_pfready, 0, sizeof(uint32_t) * MOE_MAX_EXPERTS));
+      const uint64_t st_elems = (uint64_t)ns * c->slot_bytes / 2;
+      if (!encode_map_2d(&c->map_stage_d, c->d_pfstage, c->d, st_elems / c->d, (uint64_t)c->d * 2, 128) ||
+          !encode_map_2d(&c->map_stage_f, c->d_pfstage, c->ffr, st_elems / c->ffr, (uint64_t)c->ffr * 2, 256))
+        return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (prefill staging area)");
+      c->pfstage_slots = ns;
+    }
+  }
   if (!c->pool_maps) {
     const uint64_t pool_elems = (uint64_t)c->pool_bytes / 2;
     if (!encode_map_2d(&c->map_pool_d, c->pool, c->d, pool_elems / c->d, (uint64_t)c->d * 2, 128) ||
@@ -1155,6 +1197,10 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   pa.T = T; pa.n = c->n; pa.K = c->K; pa.M = c->M; pa.layer = layer; pa.policy = c->policy;
   pa.miss_mode = c->miss_mode;
   pa.gw = gate_warps(c);
+  pa.zbuf = mn ? c->d_zbuf : nullptr;
+  pa.ready = c->d_ready;
+  pa.staging_base = c->Ncov * c->M;
+  pa.stage_slots = mn ? c->pfstage_slots : 0;
   pa.last_seq = c->d_last;
   pa.scratch = c->d_pfscratch;
   pa.tag = c->d_tag + (size_t)layer * c->M;
@@ -1181,19 +1227,23 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   c->issued.store(seq, std::memory_order_release);  // (the plan kernel publishes seq)
   c->tokens[layer] += (uint32_t)T;
   c->trace_count += (long long)T * c->K;
-  if (c->miss_mode == MOE_MISS_PULL) {  // first-touch experts: host store -> slots, by the SMs
-    PullJob j;
-    j.count = &c->d_plan->nblk;
-    j.expert = c->d_plan->expert;
-    j.slot = c->d_plan->slot;
-    j.gen = c->d_plan->gen;
-    j.flag = c->d_plan->wait;
-    j.hblob = c->d_hblob + (size_t)layer * c->n;
-    j.pool = c->pool;
-    j.slot_bytes = c->slot_bytes;
-    j.ready = c->d_ready;
-    j.done = c->d_pull_done;
-    CUDA_TRY(launch_pull(j, c->num_sms, s));
+  if (c->miss_mode == MOE_MISS_PULL) {  // experts to fill: host store -> slots, by the SMs
+    for (int stg = 0; stg < (mn ? 2 : 1); ++stg) {  // pool slots, then (M < n) staging slots
+      PullJob j{};
+      j.count = &c->d_plan->nblk;
+      j.expert = c->d_plan->expert;
+      j.slot = c->d_plan->slot;
+      j.gen = c->d_plan->gen;
+      j.flag = c->d_plan->wait;
+      j.only = c->d_plan->stage;
+      j.only_val = stg;
+      j.hblob = c->d_hblob + (size_t)layer * c->n;
+      j.pool = stg ? c->d_pfstage : c->pool;
+      j.slot_bytes = c->slot_bytes;
+      j.ready = stg ? c->d_pfready : c->d_ready;
+      j.done = c->d_pull_done;
+      CUDA_TRY(launch_pull(j, c->num_sms, s));
+    }
   }
   CUDA_TRY(launch_prefill_gather((const uint16_t*)x, c->d, c->d_plan, c->d_xg, rows_cap, s));
   // ---- tensor-core expert FFN: GEMM1 (SwiGLU) then GEMM2 (down + combine)
@@ -1208,6 +1258,9 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   ta.mode = TC_MODE_SWIGLU;
   ta.mapA = c->map_xg;
   ta.mapB = c->map_pool_d;
+  ta.has_stage = mn ? 1 : 0;
+  ta.mapB2 = c->map_stage_d;
+  ta.ready2 = c->d_pfready;
   ta.N = c->ffr; ta.K = c->d;
   ta.H = reinterpret_cast<__nv_bfloat16*>(c->d_hg);
   prof_begin(c, 1, s, &pe);
@@ -1216,6 +1269,7 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   ta.mode = TC_MODE_DOWN;
   ta.mapA = c->map_hg;
   ta.mapB = c->map_pool_f;
+  ta.mapB2 = c->map_stage_f;
   ta.N = c->d; ta.K = c->ffr;
   ta.y = y;
   prof_begin(c, 2, s, &pe);
