@@ -24,6 +24,13 @@
  *  - Single-threaded per context: calls on one ctx must not race, and all
  *    moe_layer_forward calls of one ctx must be ordered on one stream.
  *  - Decode batch = 1. bf16 values are passed as their uint16_t bit patterns.
+ *  - The decode kernel is a persistent grid of one CTA per SM whose CTAs wait on each other
+ *    (grid-wide h / pull counters; across ranks in the fused TP reduction). It is launched
+ *    non-cooperatively after an occupancy check, so while a call runs its context expects
+ *    the GPU's SMs to itself: kernels of other streams or processes that hold SMs for long
+ *    can delay its CTAs (they wait with a 60 s watchdog that traps, poisoning the context).
+ *    Set MOE_COOP=1 to have the driver check co-residency at every launch (cooperative
+ *    launch, ~2.5 us per call).
  */
 #ifndef MOE_H_
 #define MOE_H_

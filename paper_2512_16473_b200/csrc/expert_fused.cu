@@ -204,6 +204,23 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
   if (ts && ctid == 0) ts[21] = globaltimer();
 }
 
+// This CTA's loads are done: warm L2 with the first rows the NEXT call's phase A will read
+// on this CTA (its static block starts at the same row for any expert) for every way of the
+// next call's set — the routing of the next call is not known yet, so all ways are touched;
+// the bytes move while the other CTAs finish this call (HBM otherwise idles in the tail and
+// in the next call's prologue). L2 prefetch only: no effect on results.
+__device__ __forceinline__ void prefetch_next(const FusedArgs& f, int b, int G, int ffr, int d) {
+  if (!f.next_pool || f.next_rows <= 0) return;
+  const int sb = (int)((unsigned)(ffr * f.pctA) / 100u / (unsigned)G);
+  const int r0 = b * sb, nr = min(f.next_rows, sb);
+  if (nr <= 0) return;
+  for (int w = 0; w < f.next_ways; ++w) {
+    const uint8_t* slot = f.next_pool + (long long)w * f.e.slot_bytes;
+    bulk_prefetch_l2(slot + (long long)r0 * d * 2, (uint32_t)(nr * d * 2));                      // W1 rows
+    bulk_prefetch_l2(slot + (long long)(ffr + r0) * d * 2, (uint32_t)(nr * d * 2));              // W3 rows
+  }
+}
+
 constexpr int kChunkA = 2;     // phase A rows per tail claim
 constexpr int kChunkB = 1;     // phase B rows per tail claim
 
@@ -660,6 +677,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
         if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
         marker_b(kEnd);
+        prefetch_next(f, b, G, ffr, d);
         return;
       }
       for (int si = 0; si < nseg; ++si) {
@@ -693,6 +711,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       }
       if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
       marker_b(kEnd);
+      prefetch_next(f, b, G, ffr, d);
     }
     return;
   }
@@ -946,6 +965,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->pctB = p->RB <= 2 ? 10 : 20;
   p->merge = merge ? 1 : 0;
   p->prefetchB = 1;
+  p->next_rows = -1;  // (runtime default by the number of ways)
   p->hoff = hoff;
   p->hstride = hstride;
   p->smem = (size_t)NS * SB + xh + tail;
