@@ -902,6 +902,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
   }
   if (f.tpP > 0) tp_reduce_epilogue(f, b, G, ctid, nthr);
+  if (f.donef) {  // host-buffer entry point: this CTA's slice of y is in host memory
+    named_bar_sync(kPullBar, nthr);
+    if (ctid == 0) {
+      __threadfence_system();
+      f.donef[b] = f.donetag;
+    }
+  }
   if (f.ts && cw == 0 && lane == 0) {
     f.ts[b * kTsPerCta + 5] = globaltimer();
     f.ts[b * kTsPerCta + 34] = clock64();

@@ -126,6 +126,11 @@ struct FusedArgs {
   const uint16_t* xhost;
   uint32_t* xflag;
   uint32_t xseq;
+  // moe_layer_forward_host: after writing its slice of y to host memory, every CTA stores
+  // donetag into donef[blockIdx.x] (host-mapped, after a system fence); the host spins on
+  // these words instead of a CUDA event. nullptr: no flags.
+  volatile uint32_t* donef;
+  uint32_t donetag;
 };
 // Exchange buffer of one TP rank: slots[2][d][P][K] u64 at kTpSlotOff (call parity, column,
 // source rank, routing rank), each word {fp32 term w_r * o_r[c] | call tag << 32}, written

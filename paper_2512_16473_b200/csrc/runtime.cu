@@ -176,6 +176,9 @@ struct moe_ctx {
   uint32_t* d_xflag = nullptr;       // x staged by CTA 0 from host memory (zero-copy forward_host)
   uint32_t xseq = 0;
   uint8_t* d_ll1 = nullptr;          // single-rank LL slots: y written straight to host memory
+  volatile uint32_t* h_done = nullptr;  // per-CTA completion words of forward_host (host-mapped)
+  uint32_t* d_done = nullptr;
+  uint32_t done_tag = 0;
   unsigned long long ll_calls = 0;
   // profiling
   bool prof = false;
@@ -742,6 +745,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_xflag);
   cudaFree(c->d_ll1);
+  if (c->h_done) cudaFreeHost((void*)c->h_done);
   cudaFree(c->d_bar);
   cudaFree(c->d_ctr);
   cudaFree(c->d_hout);
@@ -915,7 +919,7 @@ static int gate_warps(const moe_ctx* c) { return c->fused ? 2 * c->plan.NS : kGa
 // xhost / yhost (moe_layer_forward_host, fused path): device-accessible pinned host buffers;
 // the kernel reads x from xhost into the staging buffer x and writes y straight to yhost.
 static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* y, cudaStream_t s,
-                               const uint16_t* xhost = nullptr, float* yhost = nullptr) {
+                               const uint16_t* xhost = nullptr, float* yhost = nullptr, uint32_t donetag = 0) {
   if (!c->configured) return fail(MOE_ERR_STATE, "cache_configure() has not been called");
   if (layer < 0 || layer >= c->L) return fail(MOE_ERR_INVALID_ARG, "layer out of range");
   if (!x || !y) return fail(MOE_ERR_INVALID_ARG, "NULL x or y");
@@ -1014,6 +1018,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.xhost = xhost;
     fa.xflag = c->d_xflag;
     fa.xseq = xhost ? ++c->xseq : 0u;
+    fa.donef = donetag ? c->d_done : nullptr;
+    fa.donetag = donetag;
     prof_begin(c, 1, s, &pe);
     TlRec tr;
     tl_begin(c, TL_KERNEL, seq, 0, s, &tr);
@@ -1322,9 +1328,39 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint1
     if (!c->d_ypart) CUDA_TRY(cudaMalloc(&c->d_ypart, sizeof(float) * c->d));
     CUDA_TRY(cudaDeviceSynchronize());
   }
+  // single-rank zero-copy: every CTA flags its slice of y in host memory; the host spins on
+  // those words (no driver call in the loop) instead of on a CUDA event
+  const bool flags = zc && !c->tp_fused && c->fused_grid <= 1024 && getenv("MOE_E2E_EVENT") == nullptr;
+  if (flags && !c->h_done) {
+    uint32_t* hd = nullptr;
+    CUDA_TRY(cudaHostAlloc((void**)&hd, sizeof(uint32_t) * 1024, cudaHostAllocMapped));
+    memset(hd, 0, sizeof(uint32_t) * 1024);
+    c->h_done = hd;
+    CUDA_TRY(cudaHostGetDevicePointer((void**)&c->d_done, hd, 0));
+  }
   if (zc) {
-    st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s, (const uint16_t*)xd, (float*)yd);
+    const uint32_t tag = flags ? ++c->done_tag : 0u;
+    st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s, (const uint16_t*)xd, (float*)yd, tag);
     if (st != MOE_OK) return st;
+    if (flags) {
+      CUDA_TRY(cudaEventRecord(c->host_ev, s));
+      const int G = c->fused_grid;
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int b = 0; b < G; ++b) {
+        while (c->h_done[b] != tag) {
+          // a kernel that failed never writes its flags: fall back to the event's verdict
+          if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+            cudaError_t q = cudaEventQuery(c->host_ev);
+            if (q != cudaErrorNotReady && c->h_done[b] != tag) {
+              CUDA_TRY(q);
+              return fail(MOE_ERR_CUDA, "forward_host: kernel completed without its completion flags");
+            }
+          }
+        }
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      return MOE_OK;
+    }
   } else {
     CUDA_TRY(cudaMemcpyAsync(c->d_x_e2e, x_host, sizeof(uint16_t) * c->d, cudaMemcpyHostToDevice, s));
     st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s);
