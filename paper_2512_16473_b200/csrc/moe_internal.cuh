@@ -232,7 +232,10 @@ struct TcArgs {
   CUtensorMap mapB2;           // B operand view of the prefill staging area (plan->stage blocks)
   const uint32_t* ready2;      // landed fill generation per staging slot
   int has_stage;               // mapB2 / ready2 valid
+  CUtensorMap mapBp, mapB2p;   // DOWN on CTA pairs: mapB / mapB2 with 128-row boxes
+  int has_pair_maps;
   int num_sms;                 // persistent grid size (0: the current device's SM count)
+  int pick_grid;               // grid of the one-CTA variants (the variant pick must agree across kernels)
   int mt_c2;                   // >0: both m-tiles-per-tile variants are launched and each exits
                                // unless the exact tile counts pick it (cost of a 2-m-tile tile
                                // = mt_c2/100 of a 1-m-tile one); 0: this variant runs

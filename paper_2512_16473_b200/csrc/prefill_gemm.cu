@@ -10,6 +10,7 @@
 // expert cache slots (two tensor maps view the slot pool as rows of d and of ff elements).
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "moe_internal.cuh"
 #include "tc_gemm.cuh"
@@ -299,6 +300,212 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_gemm_kernel(const __grid_con
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// The prefill GEMMs on CTA PAIRS (cta_group::2): a pair computes a 256-row x 256-column tile
+// (of both W1 and W3 for the SwiGLU GEMM, of W2 for the down GEMM) with 256 x 256 UMMAs issued
+// by the leader CTA, each CTA loading its 128 rows of the A operand (X_g / H_g) and its
+// 128-row HALF of every weight tile; each CTA's TMEM receives its 128 rows. Against one CTA
+// computing two m-tiles, every SM moves half the weight bytes of a 256-wide tile and the ring
+// gets more, smaller stages; the down GEMM's accumulators (256 columns per CTA) are
+// double-buffered, so its epilogue (the gate-weighted fp32 reductions into y) overlaps the
+// next tile's main loop.
+constexpr int kPairBN = 256;
+template <int MODE>
+struct PairCfg {
+  static constexpr int NB = MODE == TC_MODE_SWIGLU ? 2 : 1;   // weight operands per tile
+  static constexpr int kA = BM * BK * 2;                      // 16 KB: this CTA's 128 A rows
+  static constexpr int kBh = (kPairBN / 2) * BK * 2;          // 16 KB: this CTA's half of one weight tile
+  static constexpr int kStage = kA + NB * kBh;                // 48 / 32 KB
+  static constexpr int kStages = (kFusedMaxDynSmem - 2048) / kStage > 6 ? 6 : (kFusedMaxDynSmem - 2048) / kStage;
+  static constexpr int kSmem = kStages * kStage + 1024 + 256;
+  static constexpr int kAcc = NB * kPairBN;                   // TMEM columns of one accumulator set
+  static constexpr int kBufs = 2 * kAcc <= 512 ? 2 : 1;
+  static constexpr int kCols = kBufs * kAcc;
+};
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTC, 1)
+    tc_pair_kernel(const __grid_constant__ TcArgs p) {
+  using C = PairCfg<MODE>;
+  constexpr int NB = C::NB, kAcc = C::kAcc, kBufs = C::kBufs;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;      // [kBufs]
+  uint64_t* tempty = tfull + 2;              // [kBufs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // which variant runs: decided exactly as the one-CTA kernels decide it (waves of their grid
+  // times the tile cost); this kernel replaces their two-m-tile variant
+  constexpr int kBN1 = MODE == TC_MODE_SWIGLU ? 128 : 256;
+  if (p.mt_c2 > 0) {
+    const int g = p.pick_grid;
+    const int w1 = (num_tiles<1>(p, kBN1) + g - 1) / g, w2 = (num_tiles<2>(p, kBN1) + g - 1) / g;
+    if (100 * w1 < p.mt_c2 * w2) return;   // the one-m-tile kernel takes this launch
+  }
+  const int ntiles = num_tiles<2>(p, kPairBN);
+  if (pair >= ntiles) return;
+  const int ktiles = p.K / BK;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(full + s, 1);           // (the leader's: its producer's arrival + both CTAs' bytes)
+      ptx::mbar_init(empty + s, 1);          // one multicast commit of the leader's MMAs
+    }
+    for (int a = 0; a < kBufs; ++a) {
+      ptx::mbar_init(tfull + a, 1);
+      ptx::mbar_init(tempty + a, 2 * kEpiWarps);  // (the leader's: every epilogue warp of both CTAs)
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc_pair<C::kCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                            // both CTAs' barriers exist before any remote signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      prefetch_tmap(&p.mapA);
+      prefetch_tmap(&p.mapB);
+      if (p.has_stage) prefetch_tmap(&p.mapB2);
+      int it = 0;
+      for (int id = pair; id < ntiles; id += npairs) {
+        const TileCoord tc = tile_of<2>(p, kPairBN, id);
+        const bool stg = p.has_stage && p.plan->stage[tc.blk];
+        const CUtensorMap* mb = stg ? &p.mapB2 : &p.mapB;
+        if (p.plan->wait[tc.blk]) {          // expert filled by this call
+          ptx::wait_ready(stg ? p.ready2 : p.ready, p.plan->slot[tc.blk], p.plan->gen[tc.blk]);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (int kb = 0; kb < ktiles; ++kb, ++it) {
+          const int s = it % C::kStages;
+          ptx::mbar_wait(empty + s, ((it / C::kStages) & 1) ^ 1);
+          uint8_t* st = smem + (size_t)s * C::kStage;
+          if (rank == 0) ptx::mbar_arrive_expect_tx(full + s, 2u * (uint32_t)C::kStage);
+          // (a short group's second m-tile reads the following rows / TMA zero fill: unused)
+          tma_load_2d_pair(st, &p.mapA, kb * BK, tc.a_row + (int)rank * BM, full + s);
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            tma_load_2d_pair(st + C::kA + j * C::kBh, mb, kb * BK, tc.b_row[j] + (int)rank * (kPairBN / 2), full + s);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (rank == 0) {
+      const uint32_t idesc = umma_idesc_bf16(2 * BM, kPairBN);
+      int it = 0, tl = 0;
+      for (int id = pair; id < ntiles; id += npairs, ++tl) {
+        const int acc = tl % kBufs;
+        ptx::mbar_wait(tempty + acc, ((tl / kBufs) & 1) ^ 1);  // both CTAs' epilogues drained it
+        tc_fence_after();
+        const uint32_t tacc = tmem + acc * kAcc;
+        for (int kb = 0; kb < ktiles; ++kb, ++it) {
+          const int s = it % C::kStages;
+          ptx::mbar_wait(full + s, (it / C::kStages) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint8_t* st = smem + (size_t)s * C::kStage;
+            const uint64_t da = umma_desc_sw128(st);
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k)
+#pragma unroll
+              for (int j = 0; j < NB; ++j)
+                umma_bf16_pair(tacc + j * kPairBN, da + 2 * k, umma_desc_sw128(st + C::kA + j * C::kBh) + 2 * k, idesc,
+                               (kb | k) != 0);
+            umma_commit_pair(empty + s);     // the stage is free in both CTAs once these MMAs read it
+            if (kb == ktiles - 1) umma_commit_pair(tfull + acc);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quarter = warp & 3, chalf = warp >= 6 ? 1 : 0;
+    const int row = quarter * 32 + lane;
+    const int cb = chalf * (kPairBN / 2), ce = cb + kPairBN / 2;
+    int tl = 0;
+    for (int id = pair; id < ntiles; id += npairs, ++tl) {
+      const TileCoord tc = tile_of<2>(p, kPairBN, id);
+      const int acc = tl % kBufs;
+      ptx::mbar_wait(tfull + acc, (tl / kBufs) & 1);
+      tc_fence_after();
+      if ((int)rank < tc.nm) {
+        const uint32_t tbase = tmem + acc * kAcc + ((uint32_t)(quarter * 32) << 16);
+        const int orow = tc.out_row + (int)rank * BM + row;
+        if (MODE == TC_MODE_SWIGLU) {
+          for (int c = cb; c < ce; c += 32) {
+            uint32_t g[32], u[32];
+            tmem_ld32(tbase + c, g);
+            tmem_ld32(tbase + kPairBN + c, u);
+            __nv_bfloat162 hv[16];
+#pragma unroll
+            for (int q = 0; q < 32; q += 2) {
+              const float g0 = __uint_as_float(g[q]), g1 = __uint_as_float(g[q + 1]);
+              const float h0 = __fdividef(g0, 1.0f + __expf(-g0)) * __uint_as_float(u[q]);
+              const float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * __uint_as_float(u[q + 1]);
+              hv[q / 2] = __floats2bfloat162_rn(h0, h1);
+            }
+            __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.H + (size_t)orow * p.ldh + tc.out_col + c);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<const uint4*>(hv + q);
+          }
+        } else {
+          // y[token] += w * o: one addend per routed expert; K <= 2 keeps it exact
+          const int tok = p.plan->tok[orow];
+          const float w = p.plan->wrow[orow];
+          for (int c = cb; c < ce; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + c, v);
+            if (tok >= 0 && tc.out_col + c < p.N) {
+              float* dst = p.y + (size_t)tok * p.N + tc.out_col + c;
+#pragma unroll
+              for (int q = 0; q < 32; q += 4)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + q),
+                             "f"(w * __uint_as_float(v[q])), "f"(w * __uint_as_float(v[q + 1])),
+                             "f"(w * __uint_as_float(v[q + 2])), "f"(w * __uint_as_float(v[q + 3]))
+                             : "memory");
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(tempty + acc, 0));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                            // no CTA frees its TMEM while the pair still uses it
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc_pair<C::kCols>(tmem);
+  }
+}
+
+template <int MODE>
+cudaError_t preload_pair() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, tc_pair_kernel<MODE>);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(tc_pair_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<MODE>::kSmem);
+  return e;
+}
+
+template <int MODE>
+cudaError_t launch_pair(const TcArgs& q, int max_mtiles, int sms, cudaStream_t s) {
+  const int ptiles = ((q.N + kPairBN - 1) / kPairBN) * ((max_mtiles + 1) / 2);
+  const int pairs = ptiles < sms / 2 ? ptiles : sms / 2;
+  tc_pair_kernel<MODE><<<2 * pairs, kThreadsTC, PairCfg<MODE>::kSmem, s>>>(q);
+  return cudaGetLastError();
+}
+
 template <int BN, int NB, int MT>
 cudaError_t launch_tc(const TcArgs& p, int max_tiles, int num_sms, cudaStream_t s) {
   using C = TcCfg<BN, NB, MT>;
@@ -326,8 +533,15 @@ constexpr int kMtDown = 2;
 
 }  // namespace
 
+static bool pair_enabled() {  // MOE_PREFILL_PAIR=0: the one-CTA two-m-tile kernel (A/B runs)
+  const char* e = getenv("MOE_PREFILL_PAIR");
+  return !(e && e[0] == '0');
+}
+
 cudaError_t preload_tc_kernels() {
-  cudaError_t e = preload_tc<128, 1, 1>();
+  cudaError_t e = preload_pair<TC_MODE_SWIGLU>();
+  if (e == cudaSuccess) e = preload_pair<TC_MODE_DOWN>();
+  if (e == cudaSuccess) e = preload_tc<128, 1, 1>();
   if (e == cudaSuccess) e = preload_tc<128, 2, kMtSwiglu>();
   if (e == cudaSuccess) e = preload_tc<256, 1, kMtDown>();
   if (e == cudaSuccess) e = preload_tc<128, 2, 1>();
@@ -363,9 +577,16 @@ cudaError_t launch_tc_swiglu(const TcArgs& p, int max_mtiles, int mt, cudaStream
   const int tiles = ((p.N + 127) / 128) * max_mtiles;
   TcArgs q = p;
   q.mt_c2 = mt == 0 ? kC2Swiglu : 0;
+  q.pick_grid = tiles < sms ? tiles : sms;
   cudaError_t e = cudaSuccess;
   if (mt != 2) e = launch_tc<128, 2, 1>(q, tiles, sms, s);
-  if (e == cudaSuccess && mt != 1) e = launch_tc<128, 2, kMtSwiglu>(q, tiles, sms, s);
+  if (e == cudaSuccess && mt != 1) {
+    if (pair_enabled() && p.ffr % kPairBN == 0 && sms >= 2) {
+      e = launch_pair<TC_MODE_SWIGLU>(q, max_mtiles, sms, s);  // two m-tiles per tile on a CTA pair
+    } else {
+      e = launch_tc<128, 2, kMtSwiglu>(q, tiles, sms, s);
+    }
+  }
   return e;
 }
 
@@ -374,9 +595,23 @@ cudaError_t launch_tc_down(const TcArgs& p, int max_mtiles, int mt, cudaStream_t
   const int tiles = ((p.N + 255) / 256) * max_mtiles;
   TcArgs q = p;
   q.mt_c2 = mt == 0 ? kC2Down : 0;
+  q.pick_grid = tiles < sms ? tiles : sms;
   cudaError_t e = cudaSuccess;
   if (mt != 2) e = launch_tc<256, 1, 1>(q, tiles, sms, s);
-  if (e == cudaSuccess && mt != 1) e = launch_tc<256, 1, kMtDown>(q, tiles, sms, s);
+  if (e == cudaSuccess && mt != 1) {
+    // down GEMM on CTA pairs: opt-in (MOE_PREFILL_PAIR_DOWN=1) — interleaved A/B at T = 4096-8192
+    // it measured 4-5 % below the one-CTA two-m-tile kernel, which already shares each W2
+    // tile across 256 rows (the SwiGLU GEMM, two weight operands per tile, gains 10-15 %)
+    const char* pd = getenv("MOE_PREFILL_PAIR_DOWN");
+    if (pd && pd[0] == '1' && pair_enabled() && p.has_pair_maps && p.d % kPairBN == 0 && sms >= 2) {
+      TcArgs r = q;                          // weight views with 128-row boxes (half tiles)
+      r.mapB = p.mapBp;
+      r.mapB2 = p.mapB2p;
+      e = launch_pair<TC_MODE_DOWN>(r, max_mtiles, sms, s);
+    } else {
+      e = launch_tc<256, 1, kMtDown>(q, tiles, sms, s);
+    }
+  }
   return e;
 }
 

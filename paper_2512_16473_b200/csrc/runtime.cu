@@ -227,7 +227,7 @@ struct moe_ctx {
   float* d_wrow = nullptr;
   uint16_t* d_xg = nullptr;
   uint16_t* d_hg = nullptr;
-  CUtensorMap map_xg{}, map_hg{}, map_pool_d{}, map_pool_f{};
+  CUtensorMap map_xg{}, map_hg{}, map_pool_d{}, map_pool_f{}, map_pool_f128{};
   bool pool_maps = false;
   // prefill with M < n: logits of the prompt, staging area for routed experts that are not
   // resident at the end of the prompt (n - M slots), its landed generations and tensor maps
@@ -236,7 +236,7 @@ struct moe_ctx {
   uint8_t* d_pfstage = nullptr;
   int pfstage_slots = 0;
   uint32_t* d_pfready = nullptr;
-  CUtensorMap map_stage_d{}, map_stage_f{};
+  CUtensorMap map_stage_d{}, map_stage_f{}, map_stage_f128{};
   unsigned long long fused_calls = 0;
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
@@ -1118,12 +1118,9 @@ MOE_API int64_t moe_debug_stream_timeline(moe_ctx* c, double* out, int64_t cap) 
 // m-tiles per CTA tile of the prefill GEMMs: 0 = chosen on the device from the exact tile
 // counts (prefill_gemm.cu); MOE_PREFILL_MT=1|2 forces one variant (A/B runs).
 static int prefill_mt() {
-  static const int forced = [] {
-    const char* e = getenv("MOE_PREFILL_MT");
-    const int v = e ? atoi(e) : 0;
-    return v == 1 || v == 2 ? v : 0;
-  }();
-  return forced;
+  const char* e = getenv("MOE_PREFILL_MT");  // (read per call: prefill calls are few and large)
+  const int v = e ? atoi(e) : 0;
+  return v == 1 || v == 2 ? v : 0;
 }
 
 MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, float* y, int32_t T, void* stream) {
@@ -1195,7 +1192,8 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
       CUDA_TRY(cudaMemset(c->d_pfready, 0, sizeof(uint32_t) * MOE_MAX_EXPERTS));
       const uint64_t st_elems = (uint64_t)ns * c->slot_bytes / 2;
       if (!encode_map_2d(&c->map_stage_d, c->d_pfstage, c->d, st_elems / c->d, (uint64_t)c->d * 2, 128) ||
-          !encode_map_2d(&c->map_stage_f, c->d_pfstage, c->ffr, st_elems / c->ffr, (uint64_t)c->ffr * 2, 256))
+          !encode_map_2d(&c->map_stage_f, c->d_pfstage, c->ffr, st_elems / c->ffr, (uint64_t)c->ffr * 2, 256) ||
+          !encode_map_2d(&c->map_stage_f128, c->d_pfstage, c->ffr, st_elems / c->ffr, (uint64_t)c->ffr * 2, 128))
         return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (prefill staging area)");
       c->pfstage_slots = ns;
     }
@@ -1203,7 +1201,8 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   if (!c->pool_maps) {
     const uint64_t pool_elems = (uint64_t)c->pool_bytes / 2;
     if (!encode_map_2d(&c->map_pool_d, c->pool, c->d, pool_elems / c->d, (uint64_t)c->d * 2, 128) ||
-        !encode_map_2d(&c->map_pool_f, c->pool, c->ffr, pool_elems / c->ffr, (uint64_t)c->ffr * 2, 256))
+        !encode_map_2d(&c->map_pool_f, c->pool, c->ffr, pool_elems / c->ffr, (uint64_t)c->ffr * 2, 256) ||
+        !encode_map_2d(&c->map_pool_f128, c->pool, c->ffr, pool_elems / c->ffr, (uint64_t)c->ffr * 2, 128))
       return fail(MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (slot pool)");
     c->pool_maps = true;
   }
@@ -1289,6 +1288,9 @@ MOE_API moe_status moe_layer_prefill(moe_ctx* c, int32_t layer, const void* x, f
   ta.mapA = c->map_hg;
   ta.mapB = c->map_pool_f;
   ta.mapB2 = c->map_stage_f;
+  ta.mapBp = c->map_pool_f128;
+  ta.mapB2p = c->map_stage_f128;
+  ta.has_pair_maps = 1;
   ta.N = c->d; ta.K = c->ffr;
   ta.y = y;
   prof_begin(c, 2, s, &pe);

@@ -536,3 +536,25 @@ def test_launch_and_schedule_variants(tiny, monkeypatch, env):
             m.configure(ways=2, indexes=3)
             y0 = harness.run_decode(m, x)
         assert np.array_equal(y.view(np.uint32), y0.view(np.uint32))
+
+
+@pytest.mark.parametrize("mt", ["2", "0"])
+@pytest.mark.parametrize("T", [100, 300, 700])
+def test_prefill_pair_kernel_small_shape(monkeypatch, mt, T):
+    """Both prefill GEMMs on CTA pairs (cta_group::2, 256x256 pair tiles: (ff/P) % 256 == 0 for the SwiGLU
+    GEMM, d % 256 == 0 for the down GEMM) at
+    a small shape: expert blocks with an odd number of 128-row m-tiles (the pair's second CTA
+    then holds padding rows), MOE_PREFILL_MT=2 forcing the pair kernel and the device-picked
+    variant."""
+    monkeypatch.setenv("MOE_PREFILL_MT", mt)
+    monkeypatch.setenv("MOE_PREFILL_PAIR_DOWN", "1")   # (opt-in variant: keep it covered)
+    hm = harness.host_model(2, 256, 512, 8, 2)
+    x, _ = harness.hidden_states(hm, T, "uniform")
+    ref = _oracle_run(hm, x, N=hm.L, M=hm.n, warm=True)
+    y, tr, st = _prefill_run(hm, x, hm.n, True)
+    order = np.lexsort((tr["rank"], tr["layer"], tr["token"]))
+    for f in EXACT_FIELDS:
+        np.testing.assert_array_equal(tr[order][f].astype(np.int64), ref.records[f].astype(np.int64), err_msg=f)
+    worst = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
+                for t in range(T) for l in range(hm.L))
+    assert worst <= TOL, worst
