@@ -297,38 +297,63 @@ def test_tp_ff_split_emulated_on_one_gpu(P):
             assert np.abs(y[t, l] - r).max() / np.abs(r).max() <= TIGHT
 
 
-def _tp_nccl_worker(rank, world, port, q):
+def _tp_multi_gpu_worker(rank, world, port, q, mode):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    dev_i = rank % torch.cuda.device_count()   # (one GPU: both ranks time-slice cuda:0)
+    torch.cuda.set_device(dev_i)
+    # fused-peer: gloo plumbing only (the y sum runs in the decode kernel over NVLink P2P);
+    # nccl: the library's ncclAllReduce after the kernel (and for the prefill path)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2512_16473_b200 import tp
-    nid = tp.broadcast_nccl_id()
     L, d, ff, n, K, T = 2, 256, 1024, 8, 2, 5
     hm = harness.host_model(L, d, ff, n, K, tp_size=world, tp_rank=rank)
     x, _ = harness.hidden_states(hm, T, "paper")
-    with harness.open_moe(hm, device=rank, nccl_id=nid) as m:
+    nid = tp.broadcast_nccl_id() if mode == "nccl" else None
+    with harness.open_moe(hm, device=dev_i, nccl_id=nid) as m:
+        if mode == "fused-peer":
+            assert tp.connect_peers(m) == "fused-peer"
         m.configure(ways=2, indexes=L)
-        y = harness.run_decode(m, x, device=rank)
+        y = harness.run_decode(m, x, device=dev_i)
         tr = m.trace()
+        how = m.runtime_info()["tp_reduce"]
+    yp = None
+    if mode == "nccl":   # prefill (f4) on 2 GPUs: per-rank tensor-core GEMMs + NCCL sum
+        with harness.open_moe(hm, device=dev_i, nccl_id=tp.broadcast_nccl_id()) as m:
+            m.configure(ways=n, indexes=L, warm_start=True)
+            dev = torch.device("cuda", dev_i)
+            yp = np.zeros((T, L, d), np.float32)
+            for l in range(L):
+                xl = torch.from_numpy(np.ascontiguousarray(x[:, l, :]).view(np.int16)).to(dev)
+                yl = torch.empty((T, d), dtype=torch.float32, device=dev)
+                m.prefill(l, xl.data_ptr(), yl.data_ptr(), T)
+                torch.cuda.synchronize(dev)
+                yp[:, l] = yl.cpu().numpy()
     if rank == 0:
         full = harness.host_model(L, d, ff, n, K)
         ref = _oracle_run(full, x, N=L, M=2)
         err = max(float(np.abs(y[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
                   for t in range(T) for l in range(L))
         same = all(np.array_equal(tr[f].astype(np.int64), ref.records[f].astype(np.int64)) for f in EXACT_FIELDS)
-        q.put((err, same))
+        perr = 0.0 if yp is None else max(float(np.abs(yp[t, l] - ref.y[t, l]).max() / np.abs(ref.y[t, l]).max())
+                                          for t in range(T) for l in range(L))
+        q.put((err, same, how, perr))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_tp2_nccl_allreduce_multi_gpu():
-    """Real ff-split over 2 GPUs with the library's NCCL all-reduce (skipped on 1 GPU)."""
+@pytest.mark.parametrize("mode", ["fused-peer", "nccl"])
+def test_tp2_multi_gpu(mode):
+    """Real ff-split over 2 GPUs (skipped on 1 GPU): the fused peer-memory reduction inside
+    the decode kernel (gloo plumbing, no NCCL communicator) and the library's NCCL all-reduce
+    (decode and prefill). Bar: trace bit-exact vs the UNSPLIT oracle, y within 1e-4. On a
+    one-GPU box the fused-peer variant runs both ranks on cuda:0 (time-sliced; NCCL cannot put
+    two ranks on one device, so that variant skips)."""
     import socket
     import torch
     import torch.multiprocessing as mp
-    if torch.cuda.device_count() < 2:
+    if mode == "nccl" and torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -336,14 +361,15 @@ def test_tp2_nccl_allreduce_multi_gpu():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_tp_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_tp_multi_gpu_worker, args=(r, 2, port, q, mode)) for r in range(2)]
     for p in procs:
         p.start()
-    err, same = q.get(timeout=600)
+    err, same, how, perr = q.get(timeout=600)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert same and err <= TIGHT
+    assert same and err <= TIGHT and perr <= TOL
+    assert how == mode
 
 
 @pytest.mark.parametrize("N,M,policy", [(4, 2, oracle.LRU), (2, 3, oracle.LRU), (0, 2, oracle.LRU),
