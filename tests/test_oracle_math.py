@@ -164,3 +164,23 @@ def test_generated_hidden_states_realise_routing_with_margin(name, T):
             assert list(S) == list(ranked[t, l])
             srt = np.sort(z64)[::-1]
             assert np.min(srt[:c["K"]] - srt[1:c["K"] + 1]) >= 0.1
+
+
+def test_expert_ffn_independent_of_thread_count():
+    """The oracle's row-parallel loops give bit-identical results at any thread count (each
+    output row is one sequential sum): bench.py's cpu_baseline times it at 1 and all threads."""
+    import inputs
+    d, ff = 256, 512
+    W1, W3, W2 = inputs.expert_weights(0, 3, d, ff)
+    rng = np.random.default_rng(5)
+    x = inputs.f32_to_bf16(rng.standard_normal(d).astype(np.float32))
+    n0 = oracle.max_threads()
+    try:
+        oracle.set_threads(1)
+        o1, h1 = oracle.expert_ffn(W1, W3, W2, x)
+        oracle.set_threads(4)
+        o4, h4 = oracle.expert_ffn(W1, W3, W2, x)
+    finally:
+        oracle.set_threads(n0)
+    assert np.array_equal(o1.view(np.uint32), o4.view(np.uint32))
+    assert np.array_equal(h1.view(np.uint32), h4.view(np.uint32))

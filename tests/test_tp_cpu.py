@@ -147,3 +147,32 @@ def test_fused_tp_connect_gathers_ipc_handles_in_rank_order():
         assert got == want and mismatch and ok == "fused-peer"
         assert why == "rank 1: no P2P"
         assert disconnected == (rank == 0)   # the rank that did connect reverts
+
+
+def _group_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import bench
+    g = bench.Group(world)          # bench.py's N>1 plumbing: gloo, CPU tensors
+    try:
+        g.barrier()
+        q.put((rank, g.max(1.5 + rank)))
+    finally:
+        g.close()
+
+
+def test_bench_group_max_over_ranks_gloo():
+    """bench.py's multi-rank timing reduction (the device-timed region's max over ranks) over the
+    gloo group it uses for all N>1 plumbing — no NCCL needed unless the fused peer reduction
+    cannot be wired."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_group_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: 2.5, 1: 2.5}
