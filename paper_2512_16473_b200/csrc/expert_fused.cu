@@ -57,7 +57,11 @@ constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stag
 // back-off of the polls on flags other CTAs set (interleaved A/B: a pure spin was 0.1-0.25 us
 // slower per step on small shapes)
 #define MOE_POLL_BACKOFF(ns) __nanosleep(ns)
-constexpr int kPullBar = 14;              // named barrier: consumers' MOE_MISS_PULL copies done
+constexpr int kPullBar = 14;
+// A ring stage is released by every consumer warp that read it, as soon as its reads are done
+// (before the cross-warp reduction of its partials): phase A 2 warps x 2, phase B 4 warps x 1,
+// a marker by one thread x 4. The producer can refill the stage ~0.1-0.2 us earlier.
+constexpr uint32_t kEmptyArrivals = 4;              // named barrier: consumers' MOE_MISS_PULL copies done
 constexpr int kPullCtr = 16 * 8;          // bar[] word counting CTAs done pulling (every call adds G)
 
 // Packed fp32 FMA (sm_100: FFMA2): acc.{x,y} += a.{x,y} * b.{x,y}
@@ -287,8 +291,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   uint64_t* empty = full + NS;
   uint64_t* hbar = empty + NS;
   volatile int* meta = reinterpret_cast<volatile int*>(hbar + 1);
-  volatile float* part = reinterpret_cast<volatile float*>(meta + NS);   // [NS][4]
-  volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 4 * NS);  // full[2u] parity at phase B start
+  volatile float* part = reinterpret_cast<volatile float*>(meta + NS);   // [NS][2][4] (row parity)
+  volatile uint32_t* parB = reinterpret_cast<volatile uint32_t*>(part + 8 * NS);  // full[2u] parity at phase B start
   volatile int* metaN = reinterpret_cast<volatile int*>(parB + (NS >> 1));        // phase B: rows in the super-stage
   volatile float* partB = reinterpret_cast<volatile float*>(metaN + NS);          // [NS/2][2][kMaxRB][4] row partials
   const int RB = f.RB;
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, kEmptyArrivals);
     }
     mbar_init(hbar, 1);
     mbar_init(&gbar, 1);
@@ -728,6 +732,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const int4* w3 = reinterpret_cast<const int4*>(ring + (size_t)sA * SB + 2 * d);
     bool first = true;
     int pubseg = 0;                        // (h writer) first segment not yet published
+    int rc = 0;                            // rows of this stage so far (partials double-buffered)
     while (true) {
       mbar_wait(full + sA, ph);
       ph ^= 1;
@@ -751,22 +756,26 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       }
       const float gs = warp_sum(g.x + g.y);
       const float us = warp_sum(u.x + u.y);
+      // partials by row parity: the stage is released before they are combined, so the next
+      // row's partials (written after the refill) go to the other buffer; the one after that
+      // needs this warp's next release, which follows its own read of these
+      volatile float* pp = part + 8 * sA + 4 * (rc++ & 1);
       if (lane == 0) {
-        part[4 * sA + 2 * half] = gs;
-        part[4 * sA + 2 * half + 1] = us;
+        pp[2 * half] = gs;
+        pp[2 * half + 1] = us;
+        mbar_arrive_cnt(empty + sA, 2);    // this half's reads of the stage are done
       }
-      named_bar_sync(2 + sA, 64);          // both halves of stage sA done (reads + partials)
+      named_bar_sync(2 + sA, 64);          // both halves' partials written
       if (half == 0 && lane == 0) {
-        const float gg = part[4 * sA + 0] + part[4 * sA + 2];   // fixed order: half 0 + half 1
-        const float uu = part[4 * sA + 1] + part[4 * sA + 3];
-        mbar_arrive(empty + sA);           // (partials read first: half 1 rewrites them next row)
+        const float gg = pp[0] + pp[2];    // fixed order: half 0 + half 1
+        const float uu = pp[1] + pp[3];
         a.h[(long long)r * ffr + h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
       }
     }
     if (half == 0 && lane == 0)            // the rest of this stage's segments
       for (const int nseg = snseg; pubseg < nseg; ++pubseg) red_release_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
     named_bar_sync(2 + sA, 64);
-    if (half == 0 && lane == 0) mbar_arrive(empty + sA);  // release the end marker's stage
+    if (lane == 0) mbar_arrive_cnt(empty + sA, 2);  // release the end marker's stage (both halves)
     if (half == 0 && lane == 0 && (sA & 1) == 0) {
       parB[sA >> 1] = ph;                  // full[sA] parity for phase B
       mbar_arrive(pairbar + (sA >> 1));    // (release; merged phase B starts without a CTA barrier)
@@ -833,7 +842,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         if (f.ts && cw == 0 && lane == 0 && !f.ts[b * kTsPerCta + 15]) f.ts[b * kTsPerCta + 15] = globaltimer();
         if (m < 0) {                       // kSegB (next expert) or kEnd
           named_bar_sync(bid, 128);
-          if (q == 0 && lane == 0) mbar_arrive(empty + s);
+          if (q == 0 && lane == 0) mbar_arrive_cnt(empty + s, kEmptyArrivals);
           break;
         }
         const int r = m >> 24, c = m & 0xFFFFFF;  // expert (routing rank), first row
@@ -858,13 +867,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           const float sum = warp_sum(acc.x + acc.y);
           if (lane == 0) pb[4 * i + q] = sum;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cnt(empty + s, 1);  // this quarter's reads of the stage are done
         named_bar_sync(bid, 128);          // the 4 quarters of these rows are done
         if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 23] = globaltimer();  // (last: final B chunk)
         if (q == 0) {                      // lane i combines row i in a fixed order
           float o = 0.f;
           if (lane < nr) o = ((pb[4 * lane] + pb[4 * lane + 1]) + pb[4 * lane + 2]) + pb[4 * lane + 3];
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty + s);  // (partials read first: the next rows rewrite them)
           if (lane < nr) {
             if (f.tpP > 0) tp_push(f, r, c + lane, w * o);  // f3 / LL: straight to every rank
             else if (K == 1) a.y[c + lane] = w * o;
@@ -941,7 +950,7 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   if (K > 2 || grid < K) return false;          // deterministic combine needs K <= 2
   const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
   if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
-  const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 16 + kMaxNS * 4 + kMaxNS * 4 +
+  const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 32 + kMaxNS * 4 + kMaxNS * 4 +
                    (kMaxNS / 2) * 2 * kMaxRB * 16 + 64;
   const int xh1 = ((max(2 * d, ffr * 4) + 127) / 128) * 128;  // x (bf16) | one expert's h (fp32)
   const int hoff = ((2 * d + 127) / 128) * 128, hstride = ((ffr * 4 + 127) / 128) * 128;

@@ -27,6 +27,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
 // Waiting threads are suspended in try_wait until the phase completes (or the hint expires),
 // instead of re-issuing it: spinning waiters competed with the router warp's shared-memory
 // and shuffle traffic (MOE_MBAR_SPIN=1 restores the spin for A/B runs).
