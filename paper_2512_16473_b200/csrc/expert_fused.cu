@@ -620,7 +620,14 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           ++t;
         };
         unsigned c1 = atomicAdd(cA, (unsigned)kChunkA);
-        for (int j = sa.s0; j < sa.s1; ++j) issue_a(j);
+        for (int j = sa.s0; j < sa.s1; ++j) {
+          if (f.pfA > 0 && j + f.pfA < sa.s1) {  // L2 prefetch pfA rows ahead (static block)
+            const uint8_t* p1 = base + (long long)(j + f.pfA) * d * 2;
+            bulk_prefetch_l2(p1, 2u * d);
+            bulk_prefetch_l2(p1 + (long long)ffr * d * 2, 2u * d);
+          }
+          issue_a(j);
+        }
         unsigned c2 = atomicAdd(cA, (unsigned)kChunkA);
         while (sa.tail0 + (int)c1 < ffr) {
           const int j0 = sa.tail0 + (int)c1, j1 = min(j0 + kChunkA, ffr);
@@ -677,6 +684,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
             e1 = e2;
             if (sbk.tail0 + (int)e1 < d) e2 = atomicAdd(cB, (unsigned)RB);
             issue_b(r, r0, r1 - r0);
+            if (f.pfB && sbk.tail0 + (int)e1 < d) {  // the next claim's rows towards L2
+              const int q0 = sbk.tail0 + (int)e1, q1 = min(q0 + RB, d);
+              bulk_prefetch_l2(sbase[r] + w2off + (long long)q0 * rowB, (uint32_t)((q1 - q0) * rowB));
+            }
           }
         }
         if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
@@ -711,6 +722,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           c1 = c2;
           if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(cB, (unsigned)RB);
           issue_b(r0, r1 - r0);
+          if (f.pfB && sbk.tail0 + (int)c1 < d) {  // the next claim's rows towards L2
+            const int q0 = sbk.tail0 + (int)c1, q1 = min(q0 + RB, d);
+            bulk_prefetch_l2(w2 + (long long)q0 * rowB, (uint32_t)((q1 - q0) * rowB));
+          }
         }
       }
       if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
@@ -982,6 +997,11 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->merge = merge ? 1 : 0;
   p->prefetchB = 1;
   p->next_rows = -1;  // (runtime default by the number of ways)
+  // L2 prefetch ahead of the ring (interleaved A/B): phase-A static rows 10 / 20 ahead cost
+  // +1.5-10 us (off); the next phase-B claim's rows: Phi -0.56 us, 8x22B P = 4 -0.13, but
+  // Mixtral's single 28 KB rows +0.45 -> on only with multi-row chunks
+  p->pfA = 0;
+  p->pfB = p->RB >= 2 ? 1 : 0;
   p->hoff = hoff;
   p->hstride = hstride;
   p->smem = (size_t)NS * SB + xh + tail;

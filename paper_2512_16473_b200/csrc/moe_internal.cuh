@@ -107,6 +107,7 @@ struct FusedArgs {
   int RB;                         // W2 rows per phase-B super-stage
   int merge;                      // 1: merged phase B when every routed expert is resident and ready
   int prefetchB;                  // 1: L2 prefetch of the first W2 rows at the end of phase A
+  int pfA, pfB;                   // L2 prefetch: phase-A static rows pfA ahead; phase-B next claim
   const uint8_t* next_pool;       // != nullptr: at its end, each CTA prefetches into L2 the first
   int next_ways, next_rows;       //   next_rows W1/W3 row pairs of its static block of every way
                                   //   of the NEXT call's set (slots from next_pool, stride slot_bytes)
@@ -138,7 +139,7 @@ struct FusedArgs {
 constexpr int kTpSlotOff = 256;
 inline long long tp_xchg_bytes(int P, int K, int d) { return kTpSlotOff + 2ll * P * K * d * 8; }
 struct FusedPlan {
-  int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, prefetchB, next_rows, hoff, hstride;
+  int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, prefetchB, next_rows, pfA, pfB, hoff, hstride;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

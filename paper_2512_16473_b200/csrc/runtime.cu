@@ -660,6 +660,10 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       if (pb && atoi(pb) >= 0 && atoi(pb) <= 100) c->plan.pctB = atoi(pb);
       const char* pfb = getenv("MOE_PREFETCH_B");  // L2 prefetch of the first W2 rows (default on)
       if (pfb && pfb[0] == '0') c->plan.prefetchB = 0;
+      const char* pa2 = getenv("MOE_PF_AHEAD_A");     // phase-A static rows prefetched ahead into L2
+      if (pa2 && atoi(pa2) >= 0) c->plan.pfA = atoi(pa2);
+      const char* pb2 = getenv("MOE_PF_AHEAD_B");     // phase-B: the next claim's rows into L2
+      if (pb2) c->plan.pfB = pb2[0] == '1';
       const char* pfn = getenv("MOE_PREFETCH_NEXT");  // rows of the next call's set warmed in L2
       if (pfn && atoi(pfn) >= 0) c->plan.next_rows = atoi(pfn);
       const char* mg = getenv("MOE_MERGE");   // merged phases (default: when the plan allows)
@@ -993,6 +997,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.RB = c->plan.RB;
     fa.merge = c->plan.merge;
     fa.prefetchB = c->plan.prefetchB;
+    fa.pfA = c->plan.pfA;
+    fa.pfB = c->plan.pfB;
     {  // the next call in decode order is layer + 1 (wrapping: the next token's layer 0)
       const int nl = (layer + 1) % c->L;
       // default: one row pair per way when the set has at most 8 ways (interleaved A/B, warm:
