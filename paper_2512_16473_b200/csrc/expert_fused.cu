@@ -52,7 +52,7 @@ constexpr int kRouterWarp = 1 + kWarpsPerStage * kMaxNS;  // warp 0 producer, 1.
 constexpr int kRouteBar = 13;              // named barrier: partial logits -> router warp
 constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
-constexpr int kTsPerCta = 40;             // debug timestamps per CTA (MOE_DEBUG_TS)
+constexpr int kTsPerCta = 48;             // debug timestamps per CTA (MOE_DEBUG_TS)
 constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stage
 // back-off of the polls on flags other CTAs set (interleaved A/B: a pure spin was 0.1-0.25 us
 // slower per step on small shapes)
@@ -126,6 +126,50 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_relaxed_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Relaxed h publication. A gpu-scope release (MEMBAR.GPU) inside this streaming kernel waits
+// for the SM's outstanding memory traffic — the ring's bulk loads: ~4 us per release measured
+// under a 705 MB stream (tools/fence_cost.cu), and the grid-wide h was complete only at the
+// slowest of G x NS such releases (+2-6 us after the stages' last rows). Instead: every h
+// word of a call's buffer (double-buffered by call parity) is armed with kHUnset during the
+// previous call, writers store h with plain stores and count their segments with relaxed
+// REDs (a hint: "probably complete"), and a reader that copied h into shared memory re-reads
+// from L2 every word still carrying kHUnset until it is written. kHUnset (0xffffffff, a
+// negative NaN) is never produced by arithmetic (the canonical NaN is 0x7fffffff), and aligned
+// 4-byte stores are single-copy atomic, so a word is either armed or final.
+constexpr uint32_t kHUnset = 0xffffffffu;
+constexpr int kYCtr = 16 * 9;             // bar[] word: CTAs whose y slice is zeroed (every call adds G)
+
+__device__ __forceinline__ float ld_relaxed_f32(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+// h words [0, n) of a shared-memory copy (thread t of nt): re-read every still-armed word from
+// `src` (L2) until it is written
+__device__ __forceinline__ void settle_h(float* dst, const float* src, int n, int t, int nt) {
+  for (int i = 4 * t; i < n; i += 4 * nt) {
+    float4 v = *reinterpret_cast<const float4*>(dst + i);
+    if (__float_as_uint(v.x) == kHUnset || __float_as_uint(v.y) == kHUnset || __float_as_uint(v.z) == kHUnset ||
+        __float_as_uint(v.w) == kHUnset) {
+      const unsigned long long t0 = globaltimer();
+      for (int k = 0; k < 4; ++k) {
+        float w = dst[i + k];
+        while (__float_as_uint(w) == kHUnset) {
+          w = ld_relaxed_f32(src + i + k);
+          if (__float_as_uint(w) == kHUnset) {
+            MOE_POLL_BACKOFF(32);
+            if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+          }
+        }
+        dst[i + k] = w;
+      }
+    }
+  }
 }
 
 // spin until *p >= target (acquire); 60 s -> trap
@@ -280,7 +324,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ int rS[kMaxFusedK];                          // routing scratch (route_decide)
   __shared__ float rZ[MOE_MAX_EXPERTS], rW[kMaxFusedK];
   __shared__ __align__(8) uint64_t gbar, xbar, rbar, wbar;  // gate rows / x landed; slots / weights published
-  __shared__ __align__(8) uint64_t hbarK[kMaxFusedK];     // merged phase B: h_r landed (router warp's copy)
+  __shared__ __align__(8) uint64_t hbarK[kMaxFusedK];     // merged phase B: h_r landed and settled (router warp)
+  __shared__ __align__(8) uint64_t hrawK[kMaxFusedK];     // merged phase B: h_r's bulk copy landed
+  __shared__ __align__(8) uint64_t ybar;                  // segmented phase B: every CTA's y slice zeroed
   __shared__ __align__(8) uint64_t pairbar[kMaxNS / 2];  // merged phase B: pair u's even stage left phase A
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
@@ -305,6 +351,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   const long long w2off = 2ll * ffr * d * 2;    // W2 offset in a slot
   // bar[r] counts per-stage publications of h_r: G CTAs x NS stages per call
   const unsigned long long bar_target = (f.calls + 1) * (unsigned long long)G * (unsigned long long)NS;
+  float* const hcur = f.hf + (long long)(f.calls & 1) * K * ffr;   // this call's h (relaxed publication)
   // work-claim counters of this call ([A r][B r]); the other parity is zeroed for the next
   unsigned* ctr = f.ctr + (f.calls & 1) * (2 * kMaxFusedK);
   // the ring is free until the route is known: it stages the gate rows and x first
@@ -339,16 +386,37 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(&xbar, 1);
     mbar_init(&rbar, 32);  // every router lane arrives after its own shared-memory writes
     mbar_init(&wbar, 32);
-    for (int r = 0; r < kMaxFusedK; ++r) mbar_init(hbarK + r, 1);
+    mbar_init(&ybar, 1);
+    for (int r = 0; r < kMaxFusedK; ++r) {
+      mbar_init(hbarK + r, 32);             // merged: every router lane after settling its words
+      mbar_init(hrawK + r, 1);              // merged: the bulk copy of h_r landed
+    }
     for (int u = 0; u < kMaxNS / 2; ++u) mbar_init(pairbar + u, 1);
     fence_mbar_init();
     // the gate rows are weights, constant across calls: stream them in before the PDL wait
     const uint64_t pl = policy_evict_last();
     mbar_arrive_expect_tx(&gbar, (uint32_t)n * 2u * d);
     for (int e = 0; e < n; ++e) bulk_g2s(ring + (size_t)e * gstride, f.r.Wg + (size_t)e * d, 2u * d, &gbar, pl);
+    // L2 prefetches while the previous call drains (hints only: L2 is coherent, so a line the
+    // previous kernel still writes is never served stale): x, and this CTA's first row pairs
+    // of every way of the set (the route is not known yet)
+    if (f.pfx && !f.xhost) bulk_prefetch_l2(f.e.x, 2u * d);
+    if (f.cur_pool && f.start_rows > 0) {
+      const int sb = (int)((unsigned)(f.e.ffr * f.pctA) / 100u / (unsigned)gridDim.x);
+      const int r0 = blockIdx.x * sb, nr = min(f.start_rows, sb);
+      if (nr > 0)
+        for (int w = 0; w < f.cur_ways; ++w) {
+          const uint8_t* slot = f.cur_pool + (long long)w * f.e.slot_bytes;
+          bulk_prefetch_l2(slot + (long long)r0 * d * 2, (uint32_t)(nr * d * 2));
+          bulk_prefetch_l2(slot + (long long)(f.e.ffr + r0) * d * 2, (uint32_t)(nr * d * 2));
+        }
+    }
   }
   if (threadIdx.x == 32) ra = f.r;  // kernel parameters -> shared memory before the PDL wait
   __syncthreads();          // mbarrier inits and routing arguments visible
+#ifdef MOE_EARLY_TRIGGER
+  griddep_launch_dependents();
+#endif
   const int nwc = kWarpsPerStage * NS;
   // Programmatic dependent launch: the previous call's kernel (cache directory, counters,
   // h) and the caller's x are complete and visible after this wait.
@@ -383,11 +451,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   }
   if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
     f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
-  if (K == 2 && cw >= 0 && cw < nwc) {  // y accumulates the two experts: zero this CTA's slice
-                                        // (published to the other CTAs with its h releases)
-    const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
-    for (int c = c0 + ctid; c < c1; c += nthr) a.y[c] = 0.f;
-  }
   unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
   if (cw >= 0 && cw < nwc) {
     mbar_wait(&xbar, 0);
@@ -450,9 +513,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         pull_copy(const_cast<uint8_t*>(sbase[r]), ra.hblob[sexp[r]], u0, u1, ctid, nthr);
       }
       if (any) named_bar_sync(kPullBar, nthr);  // (uniform: every consumer read the same route)
+      // one arrival per CTA and call (the counter's target is (calls + 1) * G); a release only
+      // when this CTA copied bytes (a gpu-scope release costs microseconds here)
+      if (ctid == 0) {
+        if (any) red_release_add_u64(f.bar + kPullCtr, 1ull);
+        else red_relaxed_add_u64(f.bar + kPullCtr, 1ull);
+      }
+    } else if (ctid == 0) {
+      red_relaxed_add_u64(f.bar + kPullCtr, 1ull);
     }
-    // one arrival per CTA and call, in every mode (the counter's target is (calls + 1) * G)
-    if (ctid == 0) red_release_add_u64(f.bar + kPullCtr, 1ull);
   } else if (warp == kRouterWarp) {
     // ---------------------------------------------------------------- router warp
     // routing decision (route_core.cuh), identical in every CTA; CTA 0 writes its effects.
@@ -551,23 +620,52 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // miss mailbox entry (host-mapped: seq after its payload, P:200's trigger) and progress word
     if (lane == 0 && writer) publish_progress(ra, nmiss);
     griddep_launch_dependents();
+    {
+      // this CTA's slice of y (K == 2: the experts' terms accumulate onto 0) and its share of
+      // the other parity's h buffer (armed for the next call), then one release: the
+      // consumers of every CTA acquire it before their first y reduction. Off the critical
+      // path: phase B starts at least one phase A later.
+      const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
+      if (K == 2)
+        for (int c = c0 + lane; c < c1; c += 32) a.y[c] = 0.f;
+      const int hn = K * ffr;
+      uint32_t* hnext = reinterpret_cast<uint32_t*>(f.hf + (long long)((f.calls + 1) & 1) * hn);
+      const int h0 = (int)((long long)hn * b / G), h1 = (int)((long long)hn * (b + 1) / G);
+      for (int i = h0 + lane; i < h1; i += 32) hnext[i] = kHUnset;
+      __syncwarp();
+      if (lane == 0) {
+        red_release_add_u64(f.bar + kYCtr, 1ull);
+        if (!smerged) {                    // segmented phase B: acquire every CTA's zeroing here,
+          wait_counter(f.bar + kYCtr, (f.calls + 1) * (unsigned long long)G);  // off the h load's path
+          mbar_arrive(&ybar);
+        }
+      }
+    }
     __syncwarp();                          // (sorder / smerged written by other router lanes)
-    if (lane == 0 && smerged) {
+    if (smerged) {
       // merged phase B: bring every expert's h into its own buffer as soon as it is published
-      // grid-wide (the buffers lie past x: no phase-A reader is disturbed)
+      // grid-wide (the buffers lie past x: no phase-A reader is disturbed); the y zeroing of
+      // every CTA is acquired first (the consumers' reductions follow the h arrivals)
+      if (lane == 0) wait_counter(f.bar + kYCtr, (f.calls + 1) * (unsigned long long)G);
       for (int si = 0; si < K; ++si) {
         const int r = sorder[si];
-        const unsigned long long* bar = f.bar + 16 * r;
-        const unsigned long long t0 = globaltimer();
-        while (ld_acquire_u64(bar) < bar_target) {
-          MOE_POLL_BACKOFF(64);
-          if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+        float* hs = reinterpret_cast<float*>(xh + f.hoff + (size_t)r * f.hstride);
+        const float* hg = hcur + (long long)r * ffr;
+        if (lane == 0) {
+          const unsigned long long* bar = f.bar + 16 * r;
+          const unsigned long long t0 = globaltimer();
+          while (ld_acquire_u64(bar) < bar_target) {
+            MOE_POLL_BACKOFF(64);
+            if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
+          }
+          if (f.ts) f.ts[b * kTsPerCta + 19 + si] = globaltimer();  // h of segment si published grid-wide
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          mbar_arrive_expect_tx(hrawK + r, (uint32_t)ffr * 4u);
+          bulk_g2s(hs, hg, (uint32_t)ffr * 4u, hrawK + r, policy_evict_first());
         }
-        if (f.ts) f.ts[b * kTsPerCta + 19 + si] = globaltimer();  // h of segment si published grid-wide
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        mbar_arrive_expect_tx(hbarK + r, (uint32_t)ffr * 4u);
-        bulk_g2s(xh + f.hoff + (size_t)r * f.hstride, a.h + (long long)r * ffr, (uint32_t)ffr * 4u, hbarK + r,
-                 policy_evict_first());
+        mbar_wait(hrawK + r, 0);
+        settle_h(hs, hg, ffr, lane, 32);   // words whose store had not reached L2 yet
+        mbar_arrive(hbarK + r);            // (count 32: each lane after its own settled words)
       }
     }
     return;
@@ -582,7 +680,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       mbar_wait(&rbar, 0);                            // route published by the router warp
       const int nseg = snseg;
       for (int r = 0; r < K; ++r)  // host-computed experts have no h: publish them at once
-        if (shost[r]) red_release_add_u64(f.bar + 16 * r, (unsigned long long)NS);
+        if (shost[r]) red_relaxed_add_u64(f.bar + 16 * r, (unsigned long long)NS);
       uint32_t use = 0;                               // per-stage use-count parity bits
       auto acquire = [&](int s) {                     // wait until stage s is free
         mbar_wait(empty + s, ((use >> s) & 1) ^ 1);
@@ -617,6 +715,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           mbar_arrive_expect_tx(full + s, (uint32_t)rowA);
           bulk_g2s(ring + (size_t)s * SB, w1, 2u * d, full + s, pol);
           bulk_g2s(ring + (size_t)s * SB + 2 * d, w3, 2u * d, full + s, pol);
+          if (f.ts && t == 0) f.ts[b * kTsPerCta + 38] = globaltimer();  // first weight row issued
           ++t;
         };
         unsigned c1 = atomicAdd(cA, (unsigned)kChunkA);
@@ -759,7 +858,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       // row of the earlier segments it produced; publish them (release at gpu scope covers
       // its own stores)
       if (half == 0 && lane == 0)
-        for (; pubseg < si; ++pubseg) red_release_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+        for (; pubseg < si; ++pubseg) {
+          if (f.ts && sA == 0 && pubseg == 0) f.ts[b * kTsPerCta + 39] = globaltimer();
+          red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+          if (f.ts && sA == 0 && pubseg == 0) f.ts[b * kTsPerCta + 40] = globaltimer();
+        }
       if (f.ts && first && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 2] = globaltimer();
       first = false;
       float2 g = make_float2(0.f, 0.f), u = make_float2(0.f, 0.f);
@@ -784,11 +887,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       if (half == 0 && lane == 0) {
         const float gg = pp[0] + pp[2];    // fixed order: half 0 + half 1
         const float uu = pp[1] + pp[3];
-        a.h[(long long)r * ffr + h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
+        hcur[(long long)r * ffr + h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
       }
     }
     if (half == 0 && lane == 0)            // the rest of this stage's segments
-      for (const int nseg = snseg; pubseg < nseg; ++pubseg) red_release_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+      for (const int nseg = snseg; pubseg < nseg; ++pubseg) {
+        if (f.ts && sA == 0) f.ts[b * kTsPerCta + 41 + 2 * pubseg] = globaltimer();
+        red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+        if (f.ts && sA == 0) f.ts[b * kTsPerCta + 42 + 2 * pubseg] = globaltimer();
+      }
     named_bar_sync(2 + sA, 64);
     if (lane == 0) mbar_arrive_cnt(empty + sA, 2);  // release the end marker's stage (both halves)
     if (half == 0 && lane == 0 && (sA & 1) == 0) {
@@ -802,7 +909,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   // (the async proxy reads global memory written through the generic proxy by other CTAs:
   // fence the proxies first).
   uint32_t hph = 0;
-  auto load_h = [&](int r, bool) {
+  auto load_h = [&](int r, bool first_h) {
     named_bar_sync(1, nthr);
     if (cw == 0 && lane == 0) {
       const unsigned long long* bar = f.bar + 16 * r;
@@ -816,12 +923,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
       }
       if (dbg) f.ts[b * kTsPerCta + 17] = globaltimer();  // first h published grid-wide
+      if (first_h) mbar_wait(&ybar, 0);    // y zeroed by every CTA (acquired by the router warp)
       asm volatile("fence.proxy.async.global;" ::: "memory");
       mbar_arrive_expect_tx(hbar, (uint32_t)ffr * 4u);
-      bulk_g2s(xh, a.h + (long long)r * ffr, (uint32_t)ffr * 4u, hbar, policy_evict_first());
+      bulk_g2s(xh, hcur + (long long)r * ffr, (uint32_t)ffr * 4u, hbar, policy_evict_first());
     }
     mbar_wait(hbar, hph);
     hph ^= 1;
+    settle_h(reinterpret_cast<float*>(xh), hcur + (long long)r * ffr, ffr, ctid, nthr);
+    named_bar_sync(1, nthr);               // every settled word visible to every consumer
   };
   const int nseg = snseg;                  // (visible: published before the producer's first marker)
   const bool mm = smerged;                 // merged phase B: one pass over every expert
@@ -845,7 +955,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           ph = parB[u];
         }
       } else {
-        load_h(sorder[si], false);
+        load_h(sorder[si], si == 0);
         if (si == 0 && active) ph = parB[u];  // written before load_h's barrier
       }
       if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + (si == 0 ? 4 : 6)] = globaltimer();
@@ -903,8 +1013,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   for (int r = 0; r < K; ++r) {
     if (!shost[r]) continue;
     if (cw == 0 && lane == 0) {
-      // every CTA zeroed its slice of y before publishing on bar[r] (release)
-      wait_counter(f.bar + 16 * r, bar_target);
+      // every CTA zeroed its slice of y before its release on the y counter
+      wait_counter(f.bar + kYCtr, (f.calls + 1) * (unsigned long long)G);
       const uint32_t want = (uint32_t)a.seq;
       const unsigned long long t0 = globaltimer();
       unsigned ns = 256;
@@ -1002,6 +1112,8 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   // Mixtral's single 28 KB rows +0.45 -> on only with multi-row chunks
   p->pfA = 0;
   p->pfB = p->RB >= 2 ? 1 : 0;
+  p->start_rows = -1;  // (runtime default by the number of ways)
+  p->pfx = 1;
   p->hoff = hoff;
   p->hstride = hstride;
   p->smem = (size_t)NS * SB + xh + tail;

@@ -99,6 +99,7 @@ struct FusedArgs {
   RouteArgs r;                    // routing inputs (every CTA takes the decision; CTA 0 writes it)
   ExpertArgs e;
   unsigned long long* bar;        // per-expert h publication counters [K] (monotonic across calls)
+  float* hf;                      // h [2 (call parity)][K][ffr], words armed with kHUnset
   unsigned long long calls;       // number of earlier fused launches on this context
   unsigned* ctr;                  // work-claim counters [2][kMaxK] (phase A rows, phase B rows), zeroed per call
   int NS, SB;                     // ring stages / stage bytes
@@ -111,6 +112,10 @@ struct FusedArgs {
   const uint8_t* next_pool;       // != nullptr: at its end, each CTA prefetches into L2 the first
   int next_ways, next_rows;       //   next_rows W1/W3 row pairs of its static block of every way
                                   //   of the NEXT call's set (slots from next_pool, stride slot_bytes)
+  const uint8_t* cur_pool;        // != nullptr: before its PDL wait, each CTA prefetches into L2 the
+  int cur_ways, start_rows;       //   first start_rows W1/W3 row pairs of its static block of every
+                                  //   way of THIS call's set (slots from cur_pool)
+  int pfx;                        // 1: x prefetched into L2 before the PDL wait
   int hoff, hstride;              // merged: h_r at xh + hoff + r * hstride
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
@@ -140,6 +145,7 @@ constexpr int kTpSlotOff = 256;
 inline long long tp_xchg_bytes(int P, int K, int d) { return kTpSlotOff + 2ll * P * K * d * 8; }
 struct FusedPlan {
   int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, prefetchB, next_rows, pfA, pfB, hoff, hstride;
+  int start_rows, pfx;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

@@ -157,6 +157,7 @@ struct moe_ctx {
   DevStats* d_stats = nullptr;
   RouteRec* d_route = nullptr;
   float* d_h = nullptr;
+  float* d_hf = nullptr;               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
   moe_access_record* d_trace = nullptr;
   long long trace_cap = 0, trace_count = 0;
   std::vector<uint32_t> tokens;  // per-layer call count = token index
@@ -477,7 +478,7 @@ MOE_API int moe_debug_tc_gemm(const void* A, const void* B, float* C, int M, int
 MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
   if (!c || !c->d_ts) return 0;
   cudaDeviceSynchronize();
-  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * 40 * c->fused_grid, cudaMemcpyDeviceToHost);
+  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * 48 * c->fused_grid, cudaMemcpyDeviceToHost);
   return c->fused_grid;
 }
 
@@ -625,6 +626,10 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   }
   INIT_TRY(cudaMalloc(&c->d_route, sizeof(RouteRec)));
   INIT_TRY(cudaMalloc(&c->d_h, sizeof(float) * (size_t)K * c->ffr));
+  // the fused kernel's h: two buffers by call parity, every word armed with the "not yet
+  // written" pattern (expert_fused.cu: relaxed h publication)
+  INIT_TRY(cudaMalloc(&c->d_hf, sizeof(float) * 2 * (size_t)K * c->ffr));
+  INIT_TRY(cudaMemset(c->d_hf, 0xff, sizeof(float) * 2 * (size_t)K * c->ffr));
   INIT_TRY(cudaMalloc(&c->d_x_e2e, sizeof(uint16_t) * d));
   INIT_TRY(cudaMalloc(&c->d_y_e2e, sizeof(float) * d));
   INIT_TRY(cudaMalloc(&c->d_xflag, sizeof(uint32_t)));
@@ -666,6 +671,10 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       if (pb2) c->plan.pfB = pb2[0] == '1';
       const char* pfn = getenv("MOE_PREFETCH_NEXT");  // rows of the next call's set warmed in L2
       if (pfn && atoi(pfn) >= 0) c->plan.next_rows = atoi(pfn);
+      const char* pfs = getenv("MOE_PREFETCH_START");  // rows of this call's set warmed before the PDL wait
+      if (pfs && atoi(pfs) >= 0) c->plan.start_rows = atoi(pfs);
+      const char* pfx = getenv("MOE_PREFETCH_X");      // x into L2 before the PDL wait
+      if (pfx) c->plan.pfx = pfx[0] == '1';
       const char* mg = getenv("MOE_MERGE");   // merged phases (default: when the plan allows)
       if (mg && mg[0] == '0') c->plan.merge = 0;
       const char* rb = getenv("MOE_ROWS_B");  // W2 rows per phase-B super-stage (<= plan's)
@@ -682,8 +691,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_dbg, c->h_dbg, 0));
     }
     if (getenv("MOE_DEBUG_TS")) {      // per-CTA phase timestamps in device memory (cheap)
-      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 40 * c->fused_grid));
-      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 40 * c->fused_grid));
+      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 48 * c->fused_grid));
+      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 48 * c->fused_grid));
       INIT_TRY(cudaMalloc(&c->d_sts, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
       INIT_TRY(cudaMemset(c->d_sts, 0, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
     }
@@ -745,6 +754,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   cudaFree(c->d_pull_done);
   cudaFree(c->d_route);
   cudaFree(c->d_h);
+  cudaFree(c->d_hf);
   cudaFree(c->d_x_e2e);
   cudaFree(c->d_y_e2e);
   cudaFree(c->d_xflag);
@@ -987,6 +997,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.r = ra;
     fa.e = ea;
     fa.bar = c->d_bar;
+    fa.hf = c->d_hf;
     fa.calls = c->fused_calls;
     fa.ctr = c->d_ctr;
     fa.NS = c->plan.NS;
@@ -1004,11 +1015,21 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
       // default: one row pair per way when the set has at most 8 ways (interleaved A/B, warm:
       // Mixtral -0.57 us, 8x22B P = 4 / 8 slices -0.57 / -0.42; with Phi's 16 ways the 38 MB of
       // mostly unused rows cost +0.38 us); MOE_PREFETCH_NEXT=rows overrides (0 = off)
-      const int rows = c->plan.next_rows >= 0 ? c->plan.next_rows : (c->M <= 8 ? 1 : 0);
+      const int rows = c->plan.next_rows >= 0 ? c->plan.next_rows : 0;
       const bool ok = rows > 0 && nl < c->Ncov && c->miss_mode != MOE_MISS_HOST_COMPUTE;
       fa.next_pool = ok ? c->pool + (long long)nl * c->M * c->slot_bytes : nullptr;
       fa.next_ways = c->M;
       fa.next_rows = rows;
+    }
+    {
+      // default: one row pair per way of a set with at most 8 ways, issued by each CTA before
+      // its PDL wait (the bytes land while the previous call drains and this one routes)
+      const int rows = c->plan.start_rows >= 0 ? c->plan.start_rows : (c->M <= 8 ? 1 : 0);
+      const bool ok = rows > 0 && layer < c->Ncov && c->miss_mode != MOE_MISS_HOST_COMPUTE;
+      fa.cur_pool = ok ? c->pool + (long long)layer * c->M * c->slot_bytes : nullptr;
+      fa.cur_ways = c->M;
+      fa.start_rows = rows;
+      fa.pfx = c->plan.pfx;
     }
     fa.hoff = c->plan.hoff;
     fa.hstride = c->plan.hstride;
@@ -1468,6 +1489,7 @@ static moe_status tp_reset(moe_ctx* c) {
   // grid may have changed in moe_tp_connect_local)
   CUDA_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
   CUDA_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * 2 * kMaxK));
+  CUDA_TRY(cudaMemset(c->d_hf, 0xff, sizeof(float) * 2 * (size_t)c->K * c->ffr));  // call parity restarts
   CUDA_TRY(cudaDeviceSynchronize());
   c->fused_calls = 0;
   c->tp_calls = 0;

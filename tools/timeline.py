@@ -28,13 +28,15 @@ import bench_shapes  # noqa: E402
 import harness  # noqa: E402
 import paper_2512_16473_b200 as moe  # noqa: E402
 
-# per-CTA slots written by expert_fused_kernel (kTsPerCta = 40)
+# per-CTA slots written by expert_fused_kernel (kTsPerCta = 48)
 MARKS = {0: "cta_start", 8: "pdl_wait_done", 9: "x_landed", 10: "router_has_logits", 1: "route_published",
          11: "route_decided", 2: "first_row_consumed", 3: "phase_A_done", 4: "phase_B_first_h", 6: "phase_B_second_h",
          5: "cta_end", 12: "prod_last_A_issued", 13: "prod_last_Bo0_issued", 14: "prod_last_B_issued",
          15: "first_B_row_seen", 16: "cta_out_of_phase_A", 17: "h_first_published",
          19: "merged_h0_published", 20: "merged_h1_published", 22: "merged_h1_landed_warp0",
-         23: "warp0_last_B_chunk_done"}
+         23: "warp0_last_B_chunk_done", 38: "prod_first_row_issued", 39: "st0_pub_h0_before", 40: "st0_pub_h0_after",
+         41: "st0_end_pub_seg0_before", 42: "st0_end_pub_seg0_after", 43: "st0_end_pub_seg1_before",
+         44: "st0_end_pub_seg1_after"}
 KSTS_RING, KSTS_HEAD = 64, 8
 
 
@@ -60,12 +62,12 @@ def main():
             m.forward(0, xd[i % args.tokens, 0].data_ptr(), yd[i % args.tokens].data_ptr(), s.cuda_stream)
         s.synchronize()
         G = m.runtime_info()["grid"]
-        ts = np.zeros(G * 40, np.uint64)
+        ts = np.zeros(G * 48, np.uint64)
         lib.moe_debug_timestamps(m._h.value, ts.ctypes.data)
         stride = KSTS_HEAD + 2 * G
         sts = np.zeros(KSTS_RING * stride, np.uint64)
         lib.moe_debug_step_ts(m._h.value, sts.ctypes.data)
-    ts = ts.reshape(G, 40).astype(np.int64)
+    ts = ts.reshape(G, 48).astype(np.int64)
     sts = sts.reshape(KSTS_RING, stride).astype(np.int64)
     last = args.steps  # seq of the last call (seqs start at 1)
     prev = sts[(last - 1) % KSTS_RING]
