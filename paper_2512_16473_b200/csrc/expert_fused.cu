@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   volatile int* metaN = reinterpret_cast<volatile int*>(parB + (NS >> 1));        // phase B: rows in the super-stage
   volatile float* partB = reinterpret_cast<volatile float*>(metaN + NS);          // [NS/2][2][kMaxRB][4] row partials
   const int RB = f.RB;
+  const int RBp = f.RBp;                   // partB row stride (the plan's RB; MOE_ROWS_B may lower RB)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K, d = a.d, ffr = a.ffr, n = f.r.n;
@@ -437,15 +438,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.xflag), "r"(f.xseq) : "memory");
     }
   }
-  if (threadIdx.x == 0) {
-    if (f.xhost) {                            // wait for CTA 0's copy of x
-      const unsigned long long t0 = globaltimer();
-      while ((int)(ld_acquire_u32(f.xflag) - f.xseq) < 0) {
-        MOE_POLL_BACKOFF(32);
-        if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (threadIdx.x == 0) {                    // (host entry: wait for CTA 0's copy of x first)
+    const unsigned long long t0 = globaltimer();
+    while (f.xhost && (int)(ld_acquire_u32(f.xflag) - f.xseq) < 0) {
+      MOE_POLL_BACKOFF(32);
+      if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
     }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     mbar_arrive_expect_tx(&xbar, 2u * d);
     bulk_g2s(xh, a.x, 2u * d, &xbar, policy_evict_last());
   }
@@ -453,6 +452,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
   unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
   if (cw >= 0 && cw < nwc) {
+    // x: one bulk copy into xh (measured faster than per-thread L2 loads of the GEMV's own
+    // chunks, which also had to be stored into xh for phase A)
     mbar_wait(&xbar, 0);
     if (f.ts && threadIdx.x == 32) f.ts[b * kTsPerCta + 9] = globaltimer();
     if (pm && threadIdx.x == 32) pm[1] = clock64();
@@ -642,14 +643,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       }
     }
     __syncwarp();                          // (sorder / smerged written by other router lanes)
-    if (smerged) {
+    const int nh = smerged ? K : (f.xsep && snseg > 0 ? 1 : 0);  // h buffers this warp fills
+    if (nh > 0) {
       // merged phase B: bring every expert's h into its own buffer as soon as it is published
       // grid-wide (the buffers lie past x: no phase-A reader is disturbed); the y zeroing of
       // every CTA is acquired first (the consumers' reductions follow the h arrivals)
-      if (lane == 0) wait_counter(f.bar + kYCtr, (f.calls + 1) * (unsigned long long)G);
-      for (int si = 0; si < K; ++si) {
+      // (xsep: the first segment's h into the one h buffer; the later ones are loaded by the
+      // consumers after a CTA barrier, as in the segmented mode)
+      if (lane == 0 && smerged) wait_counter(f.bar + kYCtr, (f.calls + 1) * (unsigned long long)G);
+      for (int si = 0; si < nh; ++si) {
         const int r = sorder[si];
-        float* hs = reinterpret_cast<float*>(xh + f.hoff + (size_t)r * f.hstride);
+        float* hs = reinterpret_cast<float*>(xh + f.hoff + (smerged ? (size_t)r * f.hstride : 0));
         const float* hg = hcur + (long long)r * ffr;
         if (lane == 0) {
           const unsigned long long* bar = f.bar + 16 * r;
@@ -872,12 +876,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         g = dot8_bf(w1[c], xc, g);
         u = dot8_bf(w3[c], xc, u);
       }
-      const float gs = warp_sum(g.x + g.y);
-      const float us = warp_sum(u.x + u.y);
       // partials by row parity: the stage is released before they are combined, so the next
       // row's partials (written after the refill) go to the other buffer; the one after that
       // needs this warp's next release, which follows its own read of these
       volatile float* pp = part + 8 * sA + 4 * (rc++ & 1);
+      const float gs = warp_sum(g.x + g.y);
+      const float us = warp_sum(u.x + u.y);
       if (lane == 0) {
         pp[2 * half] = gs;
         pp[2 * half + 1] = us;
@@ -909,6 +913,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   // (the async proxy reads global memory written through the generic proxy by other CTAs:
   // fence the proxies first).
   uint32_t hph = 0;
+  const int hbo = f.xsep ? f.hoff : 0;     // segmented: h over x; xsep: h beside x
   auto load_h = [&](int r, bool first_h) {
     named_bar_sync(1, nthr);
     if (cw == 0 && lane == 0) {
@@ -926,11 +931,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       if (first_h) mbar_wait(&ybar, 0);    // y zeroed by every CTA (acquired by the router warp)
       asm volatile("fence.proxy.async.global;" ::: "memory");
       mbar_arrive_expect_tx(hbar, (uint32_t)ffr * 4u);
-      bulk_g2s(xh, hcur + (long long)r * ffr, (uint32_t)ffr * 4u, hbar, policy_evict_first());
+      bulk_g2s(xh + hbo, hcur + (long long)r * ffr, (uint32_t)ffr * 4u, hbar, policy_evict_first());
     }
     mbar_wait(hbar, hph);
     hph ^= 1;
-    settle_h(reinterpret_cast<float*>(xh), hcur + (long long)r * ffr, ffr, ctid, nthr);
+    settle_h(reinterpret_cast<float*>(xh + hbo), hcur + (long long)r * ffr, ffr, ctid, nthr);
     named_bar_sync(1, nthr);               // every settled word visible to every consumer
   };
   const int nseg = snseg;                  // (visible: published before the producer's first marker)
@@ -949,7 +954,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     uint32_t seen = 0u;                    // merged: experts whose h this warp has waited for
     uint32_t nchunk = 0u;                  // chunks this pair has processed
     for (int si = 0; si < (mm ? 1 : nseg); ++si) {
-      if (mm) {                            // no CTA barrier: start once the pair's even stage is out
+      if (mm || (f.xsep && si == 0)) {     // no CTA barrier: start once the pair's even stage is out
         if (active) {
           mbar_wait(pairbar + u, 0);
           ph = parB[u];
@@ -972,18 +977,18 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
         const int r = m >> 24, c = m & 0xFFFFFF;  // expert (routing rank), first row
         const float w = swgt[r];
-        if (mm && !((seen >> r) & 1u)) {   // merged: h_r copied in by the router warp
+        if ((mm || (f.xsep && si == 0)) && !((seen >> r) & 1u)) {  // h_r copied in by the router warp
           mbar_wait(hbarK + r, 0);
           seen |= 1u << r;
           if (f.ts && cw == 0 && lane == 0 && r == sorder[1 % nseg]) f.ts[b * kTsPerCta + 22] = globaltimer();
         }
         // h_r[8k .. 8k+3] / h_r[8k+4 .. 8k+7] (2-plane layout)
-        const float4* hp0 = reinterpret_cast<const float4*>(xh + (mm ? f.hoff + (size_t)r * f.hstride : 0));
+        const float4* hp0 = reinterpret_cast<const float4*>(xh + (mm ? f.hoff + (size_t)r * f.hstride : hbo));
         const float4* hp1 = hp0 + (ffr >> 3);
         const int nr = metaN[s];           // rows c .. c+nr-1, contiguous in the stage
         // partials double-buffered by chunk parity: the next chunk's writes go to the other
         // buffer, so every write-after-read is ordered by a named barrier
-        volatile float* pb = partB + (u * 2 + (nchunk++ & 1)) * kMaxRB * 4;
+        volatile float* pb = partB + (u * 2 + (nchunk++ & 1)) * RBp * 4;
         for (int i = 0; i < nr; ++i) {
           const int4* wr = wv + i * nck;
           float2 acc = make_float2(0.f, 0.f);
@@ -1075,8 +1080,14 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   if (K > 2 || grid < K) return false;          // deterministic combine needs K <= 2
   const int SB = max(16384, 4 * d);              // one W1+W3 row pair per stage
   if (2 * ffr > 2 * SB) return false;            // a W2 row fits one super-stage (2 stages)
-  const int tail = 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 32 + kMaxNS * 4 + kMaxNS * 4 +
-                   (kMaxNS / 2) * 2 * kMaxRB * 16 + 64;
+  const int RB = min(kMaxRB, (2 * SB) / (2 * ffr));  // W2 rows per phase-B super-stage
+  // partB: [NS/2][2][RB][4]; sized for kMaxRB rows except with single-row chunks (xsep below:
+  // Mixtral's x beside h fits only with the trimmed tail) — the stage counts of the other
+  // shapes stay the measured ones (8x22B P = 2 with 8 instead of 6 stages: +1-2 us)
+  auto tail_of = [&](int rb) {
+    return 2 * kMaxNS * 8 + 8 + kMaxNS * 4 + kMaxNS * 32 + kMaxNS * 4 + kMaxNS * 4 + (kMaxNS / 2) * 2 * rb * 16 + 64;
+  };
+  const int tail = tail_of(RB == 1 ? 1 : kMaxRB);
   const int xh1 = ((max(2 * d, ffr * 4) + 127) / 128) * 128;  // x (bf16) | one expert's h (fp32)
   const int hoff = ((2 * d + 127) / 128) * 128, hstride = ((ffr * 4 + 127) / 128) * 128;
   const int xh2 = hoff + K * hstride;            // x | every expert's own h buffer (merged phase B)
@@ -1087,7 +1098,13 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   };
   // merged phase B when holding every expert's h costs no ring stage (small ff_r)
   const bool merge = K == kMaxFusedK && stages(xh2) == stages(xh1);
-  const int xh = merge ? xh2 : xh1;
+  // otherwise x and ONE h buffer side by side when that costs no ring stage either: phase B of
+  // the first expert then starts per super-stage as in the merged mode (xsep)
+  const int xh3 = hoff + hstride;
+  // (interleaved A/B: Mixtral -1.0-1.2 us, 8x22B unsplit -0.7; with multi-row W2 chunks — the
+  // P = 2 / 4 slices — +0.6-1.0 us, so only for single-row chunks)
+  const bool xsep = !merge && K == kMaxFusedK && stages(xh3) == stages(xh1) && RB == 1;
+  const int xh = merge ? xh2 : xsep ? xh3 : xh1;
   const int NS = stages(xh);
   if (NS < 4) return false;
   // the gate rows and x are staged in the (still empty) ring before the route is known
@@ -1097,7 +1114,8 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->SB = SB;
   p->NS = NS;
   p->xh_bytes = xh;
-  p->RB = min(kMaxRB, (2 * SB) / (2 * ffr));     // W2 rows per phase-B super-stage
+  p->RB = RB;
+  p->xsep = xsep ? 1 : 0;
   // static shares (rest stolen in chunks): measured on B200 across the BASELINE shapes
   // (bench_shapes.py sweeps): 95% of phase A; 10% of phase B with 1-2-row chunks, 20% with
   // bigger ones (8x22B slices) — phase B's expert switch and the end of the step leave the

@@ -106,6 +106,9 @@ struct FusedArgs {
   int xh_bytes;
   int pctA, pctB;                 // share of phase A / B rows assigned statically (rest: stolen)
   int RB;                         // W2 rows per phase-B super-stage
+  int RBp;                        // row stride of the phase-B partials (the plan's RB)
+  int xsep;                       // 1: x and one h buffer side by side (first expert's phase B
+                                  //    starts per super-stage, h copied in by the router warp)
   int merge;                      // 1: merged phase B when every routed expert is resident and ready
   int prefetchB;                  // 1: L2 prefetch of the first W2 rows at the end of phase A
   int pfA, pfB;                   // L2 prefetch: phase-A static rows pfA ahead; phase-B next claim
@@ -145,7 +148,7 @@ constexpr int kTpSlotOff = 256;
 inline long long tp_xchg_bytes(int P, int K, int d) { return kTpSlotOff + 2ll * P * K * d * 8; }
 struct FusedPlan {
   int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, prefetchB, next_rows, pfA, pfB, hoff, hstride;
-  int start_rows, pfx;
+  int start_rows, pfx, xsep;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

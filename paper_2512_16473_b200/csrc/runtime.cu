@@ -157,7 +157,8 @@ struct moe_ctx {
   DevStats* d_stats = nullptr;
   RouteRec* d_route = nullptr;
   float* d_h = nullptr;
-  float* d_hf = nullptr;               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
+  float* d_hf = nullptr;
+  int plan_RBp = 0;                    // phase-B partials row stride (plan's RB before MOE_ROWS_B)               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
   moe_access_record* d_trace = nullptr;
   long long trace_cap = 0, trace_count = 0;
   std::vector<uint32_t> tokens;  // per-layer call count = token index
@@ -675,6 +676,9 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       if (pfs && atoi(pfs) >= 0) c->plan.start_rows = atoi(pfs);
       const char* pfx = getenv("MOE_PREFETCH_X");      // x into L2 before the PDL wait
       if (pfx) c->plan.pfx = pfx[0] == '1';
+      c->plan_RBp = c->plan.RB;                   // (before MOE_ROWS_B)
+      const char* xs = getenv("MOE_XSEP");        // x beside one h buffer (default: when the plan allows)
+      if (xs && xs[0] == '0') c->plan.xsep = 0;
       const char* mg = getenv("MOE_MERGE");   // merged phases (default: when the plan allows)
       if (mg && mg[0] == '0') c->plan.merge = 0;
       const char* rb = getenv("MOE_ROWS_B");  // W2 rows per phase-B super-stage (<= plan's)
@@ -1006,6 +1010,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.pctA = c->plan.pctA;
     fa.pctB = c->plan.pctB;
     fa.RB = c->plan.RB;
+    fa.RBp = c->plan_RBp;
+    fa.xsep = c->plan.xsep;
     fa.merge = c->plan.merge;
     fa.prefetchB = c->plan.prefetchB;
     fa.pfA = c->plan.pfA;
