@@ -31,7 +31,8 @@ import inputs  # noqa: E402
 
 def epilogue_breakdown(P: int, tokens: int = 16, steps: int = 40) -> dict:
     """Median per-CTA durations (us) of the fused reduction epilogue in the last call
-    (MOE_DEBUG_TS marks 18, 21): wait for every rank's terms of the slice + fixed-order sum."""
+    (MOE_DEBUG_TS marks 18, 21): wait for every rank's terms of the slice + fixed-order sum.
+    The marks exist only in the debug build: run with MOE_LIB_PATH=.../lib/libmoe_debug.so."""
     import ctypes
     import statistics
     import torch

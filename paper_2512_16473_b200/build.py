@@ -12,6 +12,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libmoe.so")
+# the same library with the decode kernel's per-CTA debug marks compiled in (MOE_DEBUG_TS=1 with
+# MOE_LIB_PATH pointing here: tools/timeline.py, bench_tp_emul.py's epilogue breakdown)
+DEBUG_LIB = os.path.join(LIB_DIR, "libmoe_debug.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -39,7 +42,7 @@ def headers():
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(DEBUG_LIB):
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(f) > t for f in sources() + headers())
@@ -52,6 +55,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return _build_to(out, list(defines), verbose)
     if not force and not needs_build():
         return LIB
+    _build_to(DEBUG_LIB, ["MOE_DEBUG_MARKS"], False)
     return _build_to(LIB, [], verbose)
 
 

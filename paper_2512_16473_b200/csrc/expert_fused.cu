@@ -46,6 +46,18 @@ namespace {
 
 using namespace ptx;
 
+// Debug marks (per-CTA globaltimer / clock64 timestamps, stage events) exist only in the
+// debug build (-DMOE_DEBUG_MARKS, lib/libmoe_debug.so, used by tools/timeline.py): the
+// production kernel carries none of their code (a kernel this size is sensitive to its
+// instruction footprint: +1.3K SASS instructions cost Mixtral ~1 us).
+#ifdef MOE_DEBUG_MARKS
+#define TS(f) ((f).ts)
+#define STS(f) ((f).sts)
+#else
+#define TS(f) ((unsigned long long*)nullptr)
+#define STS(f) ((unsigned long long*)nullptr)
+#endif
+
 constexpr int kMaxNS = 10;                 // ring stages (phase B pairs them: NS even)
 constexpr int kWarpsPerStage = 2;          // consumer warps sharing one stage
 constexpr int kRouterWarp = 1 + kWarpsPerStage * kMaxNS;  // warp 0 producer, 1..2NS consumers
@@ -150,23 +162,35 @@ __device__ __forceinline__ float ld_relaxed_f32(const float* p) {
   return v;
 }
 // h words [0, n) of a shared-memory copy (thread t of nt): re-read every still-armed word from
-// `src` (L2) until it is written
-__device__ __forceinline__ void settle_h(float* dst, const float* src, int n, int t, int nt) {
-  for (int i = 4 * t; i < n; i += 4 * nt) {
-    float4 v = *reinterpret_cast<const float4*>(dst + i);
-    if (__float_as_uint(v.x) == kHUnset || __float_as_uint(v.y) == kHUnset || __float_as_uint(v.z) == kHUnset ||
-        __float_as_uint(v.w) == kHUnset) {
-      const unsigned long long t0 = globaltimer();
-      for (int k = 0; k < 4; ++k) {
-        float w = dst[i + k];
+// `src` (L2) until it is written. Loads are batched 8 float4 deep with one branch per batch
+// (one load-compare-branch chain per float4 made the router warp's scan of Phi's h 5 us).
+__device__ __noinline__ void settle_h(float* dst, const float* src, int n, int t, int nt) {
+  constexpr int U = 8;
+  for (int base = 4 * t; base < n; base += 4 * nt * U) {
+    float4 v[U];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = base + 4 * nt * k;
+      v[k] = i < n ? *reinterpret_cast<const float4*>(dst + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      bad |= (__float_as_uint(v[k].x) == kHUnset) | (__float_as_uint(v[k].y) == kHUnset) |
+             (__float_as_uint(v[k].z) == kHUnset) | (__float_as_uint(v[k].w) == kHUnset);
+    }
+    if (!bad) continue;
+    const unsigned long long t0 = globaltimer();
+    for (int k = 0; k < U; ++k) {
+      const int i0 = base + 4 * nt * k;
+      if (i0 >= n) break;
+      for (int e = 0; e < 4; ++e) {
+        float w = dst[i0 + e];
         while (__float_as_uint(w) == kHUnset) {
-          w = ld_relaxed_f32(src + i + k);
+          w = ld_relaxed_f32(src + i0 + e);
           if (__float_as_uint(w) == kHUnset) {
             MOE_POLL_BACKOFF(32);
             if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
           }
         }
-        dst[i + k] = w;
+        dst[i0 + e] = w;
       }
     }
   }
@@ -211,7 +235,7 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
   const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
   const int total = (c1 - c0) * PK;
   const unsigned long long tag = tp_tag(f);
-  unsigned long long* ts = f.ts ? f.ts + b * kTsPerCta : nullptr;  // debug marks 18, 21
+  unsigned long long* ts = TS(f) ? TS(f) + b * kTsPerCta : nullptr;  // debug marks 18, 21
   if (ts && ctid == 0) ts[18] = globaltimer();
   // thread i holds word j = i % PK (source rank j / K, routing rank j % K) of column
   // c0 + i / PK: poll it until it carries this call's tag, then an xor-shuffle tree over the
@@ -266,6 +290,19 @@ __device__ __forceinline__ void prefetch_next(const FusedArgs& f, int b, int G, 
     const uint8_t* slot = f.next_pool + (long long)w * f.e.slot_bytes;
     bulk_prefetch_l2(slot + (long long)r0 * d * 2, (uint32_t)(nr * d * 2));                      // W1 rows
     bulk_prefetch_l2(slot + (long long)(ffr + r0) * d * 2, (uint32_t)(nr * d * 2));              // W3 rows
+  }
+}
+
+// debug (MOE_DEBUG_TS): a stage's data was seen by its first consumer warp (time, bytes, phase)
+__device__ __forceinline__ void record_event(const FusedArgs& f, int* evn, int b, unsigned bytes, unsigned phase) {
+#ifndef MOE_DEBUG_MARKS
+  return;
+#endif
+  if (!f.ev) return;
+  const int i = atomicAdd(evn, 1);
+  if (i < kEvPerCta) {
+    f.ev[((long long)b * kEvPerCta + i) * 2] = globaltimer();
+    f.ev[((long long)b * kEvPerCta + i) * 2 + 1] = (unsigned long long)bytes | ((unsigned long long)phase << 32);
   }
 }
 
@@ -327,6 +364,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ __align__(8) uint64_t hbarK[kMaxFusedK];     // merged phase B: h_r landed and settled (router warp)
   __shared__ __align__(8) uint64_t hrawK[kMaxFusedK];     // merged phase B: h_r's bulk copy landed
   __shared__ __align__(8) uint64_t ybar;                  // segmented phase B: every CTA's y slice zeroed
+  __shared__ int evn;                                     // debug: stage events recorded this call
+  __shared__ volatile int slastA;                         // phase-A items this CTA issued (once known)
   __shared__ __align__(8) uint64_t pairbar[kMaxNS / 2];  // merged phase B: pair u's even stage left phase A
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
@@ -364,18 +403,18 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   const int nthr = kWarpsPerStage * NS * 32;
   const int ctid = threadIdx.x - 32;
 
-  if (f.sts && threadIdx.x == 0) f.sts[kStsHead + b] = globaltimer();
-  if (f.ts && threadIdx.x == 0) {
-    f.ts[b * kTsPerCta + 0] = globaltimer();
-    f.ts[b * kTsPerCta + 33] = clock64();
-    f.ts[b * kTsPerCta + 6] = 0;
-    f.ts[b * kTsPerCta + 7] = 0;
-    f.ts[b * kTsPerCta + 15] = 0;
-    f.ts[b * kTsPerCta + 16] = 0;
-    f.ts[b * kTsPerCta + 19] = 0;
-    f.ts[b * kTsPerCta + 20] = 0;
-    f.ts[b * kTsPerCta + 22] = 0;
-    f.ts[b * kTsPerCta + 23] = 0;
+  if (STS(f) && threadIdx.x == 0) STS(f)[kStsHead + b] = globaltimer();
+  if (TS(f) && threadIdx.x == 0) {
+    TS(f)[b * kTsPerCta + 0] = globaltimer();
+    TS(f)[b * kTsPerCta + 33] = clock64();
+    TS(f)[b * kTsPerCta + 6] = 0;
+    TS(f)[b * kTsPerCta + 7] = 0;
+    TS(f)[b * kTsPerCta + 15] = 0;
+    TS(f)[b * kTsPerCta + 16] = 0;
+    TS(f)[b * kTsPerCta + 19] = 0;
+    TS(f)[b * kTsPerCta + 20] = 0;
+    TS(f)[b * kTsPerCta + 22] = 0;
+    TS(f)[b * kTsPerCta + 23] = 0;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -388,6 +427,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     mbar_init(&rbar, 32);  // every router lane arrives after its own shared-memory writes
     mbar_init(&wbar, 32);
     mbar_init(&ybar, 1);
+    evn = 0;
+    slastA = 0x7fffffff;
     for (int r = 0; r < kMaxFusedK; ++r) {
       mbar_init(hbarK + r, 32);             // merged: every router lane after settling its words
       mbar_init(hrawK + r, 1);              // merged: the bulk copy of h_r landed
@@ -422,7 +463,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   // Programmatic dependent launch: the previous call's kernel (cache directory, counters,
   // h) and the caller's x are complete and visible after this wait.
   griddep_wait();
-  if (f.ts && threadIdx.x == 0) f.ts[b * kTsPerCta + 8] = globaltimer();
+  if (TS(f) && threadIdx.x == 0) TS(f)[b * kTsPerCta + 8] = globaltimer();
   DirState ds;
   if (warp == kRouterWarp) ds = dir_load(ra, lane);  // the router's directory loads in flight
   if (f.xhost && b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + nthr) {
@@ -450,12 +491,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   }
   if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
     f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
-  unsigned long long* pm = f.ts ? f.ts + b * kTsPerCta + 24 : nullptr;  // debug marks
+  unsigned long long* pm = TS(f) ? TS(f) + b * kTsPerCta + 24 : nullptr;  // debug marks
   if (cw >= 0 && cw < nwc) {
     // x: one bulk copy into xh (measured faster than per-thread L2 loads of the GEMV's own
     // chunks, which also had to be stored into xh for phase A)
     mbar_wait(&xbar, 0);
-    if (f.ts && threadIdx.x == 32) f.ts[b * kTsPerCta + 9] = globaltimer();
+    if (TS(f) && threadIdx.x == 32) TS(f)[b * kTsPerCta + 9] = globaltimer();
     if (pm && threadIdx.x == 32) pm[1] = clock64();
     // Gate GEMV z = Wg x: a few KFLOP, latency-bound — spread over every consumer
     // thread instead of a dependent chain of MMAs: thread i takes 16-B chunks i, i + nthr, ...
@@ -540,7 +581,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         if (t == lane) { way_of = w; gen_of = g; }
       }
     named_bar_sync(kRouteBar, nthr + 32);
-    if (f.ts && lane == 0) f.ts[b * kTsPerCta + 10] = globaltimer();
+    if (TS(f) && lane == 0) TS(f)[b * kTsPerCta + 10] = globaltimer();
     if (pm && lane == 0) pm[3] = clock64();
     // the shared logit order (gate_gemv.cuh): virtual warp = consumer warp, summed in order
     // (every lane sums a valid column, branch-free; lanes >= n then drop theirs)
@@ -581,7 +622,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
         mbar_arrive(&rbar);                // release (each lane its own writes): route published
         if (pm && lane == 0) pm[8] = clock64();
-        if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
+        if (TS(f) && lane == 0) TS(f)[b * kTsPerCta + 1] = globaltimer();
         published = true;
       }
     }
@@ -607,13 +648,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         smerged = f.merge && K == kMaxFusedK && __popc(dev_ready) == K;
       }
       mbar_arrive(&rbar);                  // release (each lane its own writes): route published
-      if (f.ts && lane == 0) f.ts[b * kTsPerCta + 1] = globaltimer();
+      if (TS(f) && lane == 0) TS(f)[b * kTsPerCta + 1] = globaltimer();
       published = true;
     };
     LaneRoute lr;
     const bool writer = b == 0;
     const int nmiss = route_decide(ra, z, ds, writer, rS, rZ, rW, &lr, pm ? pm + 4 : nullptr, publish);
-    if (f.ts && lane == 0) f.ts[b * kTsPerCta + 11] = globaltimer();
+    if (TS(f) && lane == 0) TS(f)[b * kTsPerCta + 11] = globaltimer();
     if (pm && lane == 0) pm[7] = clock64();
     if (!published) publish(lr);
     if (lane < K) swgt[lane] = lr.w;       // gate weights: needed from phase B on
@@ -662,13 +703,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
             MOE_POLL_BACKOFF(64);
             if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
           }
-          if (f.ts) f.ts[b * kTsPerCta + 19 + si] = globaltimer();  // h of segment si published grid-wide
+          if (TS(f)) TS(f)[b * kTsPerCta + 19 + si] = globaltimer();  // h of segment si published grid-wide
           asm volatile("fence.proxy.async.global;" ::: "memory");
           mbar_arrive_expect_tx(hrawK + r, (uint32_t)ffr * 4u);
           bulk_g2s(hs, hg, (uint32_t)ffr * 4u, hrawK + r, policy_evict_first());
         }
         mbar_wait(hrawK + r, 0);
+        if (TS(f) && lane == 0 && si == 1) TS(f)[b * kTsPerCta + 46] = globaltimer();  // h1 bulk copy landed
         settle_h(hs, hg, ffr, lane, 32);   // words whose store had not reached L2 yet
+        if (TS(f) && lane == 0 && si == 1) TS(f)[b * kTsPerCta + 47] = globaltimer();  // h1 settled
         mbar_arrive(hbarK + r);            // (count 32: each lane after its own settled words)
       }
     }
@@ -691,12 +734,24 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         use ^= 1u << s;
       };
       int t = 0;
-      auto marker_a = [&](int m) {                    // one marker into each of the NS stages
-        for (int k = 0; k < NS; ++k, ++t) {
-          const int s = t % NS;
-          acquire(s);
-          meta[s] = m;
-          mbar_arrive(full + s);
+      // Work claims: segment q = A of sorder[q] for q < nseg, B of sorder[q - nseg] after. A
+      // segment's first claim is issued before its static block; the next segment's first claim
+      // is issued ahead, while this segment's tail is within two grid-rounds of its end (the
+      // short static blocks of phase B could not hide the atomic's latency: a restart bubble)
+      unsigned pre = 0u;
+      int pre_q = -1;
+      auto seg_ctr = [&](int q) -> unsigned* {
+        return q < nseg ? ctr + sorder[q] : ctr + kMaxFusedK + sorder[q - nseg];
+      };
+      auto seg_chunk = [&](int q) -> unsigned { return q < nseg ? (unsigned)kChunkA : (unsigned)RB; };
+      auto first_claim = [&](int q) -> unsigned {
+        if (pre_q == q) return pre;
+        return atomicAdd(seg_ctr(q), seg_chunk(q));
+      };
+      auto claim_ahead = [&](int q, int tail_done, int tail_size) {  // (called with the claim just taken)
+        if (f.claim_ahead && q + 1 < 2 * nseg && pre_q != q + 1 && tail_done + 2 * G * (int)seg_chunk(q) >= tail_size) {
+          pre = atomicAdd(seg_ctr(q + 1), seg_chunk(q + 1));
+          pre_q = q + 1;
         }
       };
       // phase A: per segment, static block then tail claims (two claims in flight hide the
@@ -719,10 +774,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           mbar_arrive_expect_tx(full + s, (uint32_t)rowA);
           bulk_g2s(ring + (size_t)s * SB, w1, 2u * d, full + s, pol);
           bulk_g2s(ring + (size_t)s * SB + 2 * d, w3, 2u * d, full + s, pol);
-          if (f.ts && t == 0) f.ts[b * kTsPerCta + 38] = globaltimer();  // first weight row issued
+          if (TS(f) && t == 0) TS(f)[b * kTsPerCta + 38] = globaltimer();  // first weight row issued
           ++t;
         };
-        unsigned c1 = atomicAdd(cA, (unsigned)kChunkA);
+        unsigned c1 = first_claim(si);
         for (int j = sa.s0; j < sa.s1; ++j) {
           if (f.pfA > 0 && j + f.pfA < sa.s1) {  // L2 prefetch pfA rows ahead (static block)
             const uint8_t* p1 = base + (long long)(j + f.pfA) * d * 2;
@@ -734,33 +789,63 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         unsigned c2 = atomicAdd(cA, (unsigned)kChunkA);
         while (sa.tail0 + (int)c1 < ffr) {
           const int j0 = sa.tail0 + (int)c1, j1 = min(j0 + kChunkA, ffr);
+          claim_ahead(si, (int)c1, ffr - sa.tail0);
           c1 = c2;
           if (sa.tail0 + (int)c1 < ffr) c2 = atomicAdd(cA, (unsigned)kChunkA);
           for (int j = j0; j < j1; ++j) issue_a(j);
         }
+        if (pre_q != si + 1) claim_ahead(si, ffr, ffr);  // (a segment without a tail)
         // no marker between segments: a stage's consumers see the segment index change in
         // the row meta (its h writer then publishes the rows it wrote of the earlier
         // segment), so the ring does not drain at the expert switch
       }
-      if (f.ts) f.ts[b * kTsPerCta + 12] = globaltimer();  // last phase-A row issued
+      slastA = t;                                     // (consumers: a stage's last A row is known)
+      if (TS(f)) TS(f)[b * kTsPerCta + 12] = globaltimer();  // last phase-A row issued
       if (f.prefetchB && nseg > 0 && !swait[sorder[0]]) {
         // the ring drains before phase B starts: have this CTA's first W2 rows on their way
         // to L2 meanwhile (same bytes, read from HBM once)
         const int nr = min(NSB * RB, sbk.s1 - sbk.s0);
         if (nr > 0) bulk_prefetch_l2(sbase[sorder[0]] + w2off + (long long)sbk.s0 * rowB, (uint32_t)(nr * rowB));
       }
-      marker_a(kEnd);
       // phase B: whole W2 rows into super-stages (2u, 2u+1); W2 does not depend on h, so
-      // these loads stream while the consumers finish phase A and load h
-      int tb = 0;
+      // these loads stream while the consumers finish phase A and load h. The end-of-A markers
+      // go into a super-stage's two stages right before its first W2 rows, starting with the
+      // super-stage whose stages drain first (the ring's next stages in issue order): W2 rows
+      // enter as soon as one super-stage is free instead of after the whole ring drained.
+      int tb = f.lazy_marks ? ((t % NS) + 1) / 2 : 0;
+      uint32_t marked = 0u;
+      const int t_a = t;                              // phase-A items issued by this CTA
+      auto mark_end_a = [&](int u) {
+        if ((marked >> u) & 1u) return;
+        marked |= 1u << u;
+        for (int k = 0; k < 2; ++k) {
+          const int s = 2 * u + k;
+          acquire(s);
+          meta[s] = kEnd;
+          mbar_arrive(full + s);
+        }
+      };
       auto marker_b = [&](int m) {
         for (int k = 0; k < NSB; ++k, ++tb) {
           const int s = 2 * (tb % NSB);
+          mark_end_a(tb % NSB);
           acquire(s);
           meta[s] = m;
           mbar_arrive(full + s);
         }
       };
+      if (f.lazy_marks)                               // super-stages that got no phase-A item: at once
+        for (int u = 0; u < NSB; ++u)
+          if (2 * u >= t_a) mark_end_a(u);
+      if (!f.lazy_marks) {                            // every end-of-A marker first, in drain order
+        for (int k = 0; k < NS; ++k, ++t) {
+          const int s = t % NS;
+          acquire(s);
+          meta[s] = kEnd;
+          mbar_arrive(full + s);
+        }
+        marked = (1u << NSB) - 1u;
+      }
       if (smerged) {
         // Merged phase B (every expert resident and ready, every h resident in shared
         // memory, loaded by the router warp as soon as it is published): the experts' W2 rows
@@ -769,6 +854,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         // a warp waits for that expert's h the first time it meets it.
         auto issue_b = [&](int r, int c, int nr) {
           const int s = 2 * (tb % NSB);
+          mark_end_a(tb % NSB);
           acquire(s);
           meta[s] = (r << 24) | c;
           metaN[s] = nr;
@@ -779,11 +865,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         for (int si = 0; si < nseg; ++si) {     // experts in turn, without markers between them
           const int r = sorder[si];
           unsigned* cB = ctr + kMaxFusedK + r;
-          unsigned e1 = atomicAdd(cB, (unsigned)RB);
+          unsigned e1 = first_claim(nseg + si);
           for (int c = sbk.s0; c < sbk.s1; c += RB) issue_b(r, c, min(RB, sbk.s1 - c));
           unsigned e2 = atomicAdd(cB, (unsigned)RB);
           while (sbk.tail0 + (int)e1 < d) {
             const int r0 = sbk.tail0 + (int)e1, r1 = min(r0 + RB, d);
+            claim_ahead(nseg + si, (int)e1, d - sbk.tail0);
             e1 = e2;
             if (sbk.tail0 + (int)e1 < d) e2 = atomicAdd(cB, (unsigned)RB);
             issue_b(r, r0, r1 - r0);
@@ -793,11 +880,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
             }
           }
         }
-        if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
+        if (TS(f)) TS(f)[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
         marker_b(kEnd);
         prefetch_next(f, b, G, ffr, d);
         return;
       }
+      if (!f.xsep)                                    // segmented: every consumer loads h first
+        for (int u = 0; u < NSB; ++u) mark_end_a((tb + u) % NSB);
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* w2 = sbase[r] + w2off;
@@ -806,6 +895,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         // (small ff_r) would otherwise leave too few bytes in flight per SM
         auto issue_b = [&](int c, int nr) {
           const int s = 2 * (tb % NSB);
+          mark_end_a(tb % NSB);
           acquire(s);
           meta[s] = (r << 24) | c;
           metaN[s] = nr;
@@ -814,14 +904,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           ++tb;
         };
         if (si > 0) {
-          if (f.ts) f.ts[b * kTsPerCta + 13] = globaltimer();  // last B_o0 row issued
+          if (TS(f)) TS(f)[b * kTsPerCta + 13] = globaltimer();  // last B_o0 row issued
           marker_b(kSegB);
         }
-        unsigned c1 = atomicAdd(cB, (unsigned)RB);
+        unsigned c1 = first_claim(nseg + si);
         for (int c = sbk.s0; c < sbk.s1; c += RB) issue_b(c, min(RB, sbk.s1 - c));
         unsigned c2 = atomicAdd(cB, (unsigned)RB);
         while (sbk.tail0 + (int)c1 < d) {
           const int r0 = sbk.tail0 + (int)c1, r1 = min(r0 + RB, d);
+          claim_ahead(nseg + si, (int)c1, d - sbk.tail0);
           c1 = c2;
           if (sbk.tail0 + (int)c1 < d) c2 = atomicAdd(cB, (unsigned)RB);
           issue_b(r0, r1 - r0);
@@ -831,7 +922,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           }
         }
       }
-      if (f.ts) f.ts[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
+      if (TS(f)) TS(f)[b * kTsPerCta + 14] = globaltimer();  // last phase-B row issued
       marker_b(kEnd);
       prefetch_next(f, b, G, ffr, d);
     }
@@ -851,23 +942,26 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     bool first = true;
     int pubseg = 0;                        // (h writer) first segment not yet published
     int rc = 0;                            // rows of this stage so far (partials double-buffered)
+    int ti = sA - NS;                      // ring item index of this stage's current item
     while (true) {
+      ti += NS;
       mbar_wait(full + sA, ph);
       ph ^= 1;
       const int m = meta[sA];
       if (m < 0) break;                    // kEnd
       const int si = m >> 24, j = m & 0xFFFFFF;
       const int r = sorder[si];
+      if (half == 0 && lane == 0) record_event(f, &evn, b, (unsigned)rowA, (unsigned)si);
       // a row of a later segment: this stage's h writer (half 0, lane 0) has written every
       // row of the earlier segments it produced; publish them (release at gpu scope covers
       // its own stores)
       if (half == 0 && lane == 0)
         for (; pubseg < si; ++pubseg) {
-          if (f.ts && sA == 0 && pubseg == 0) f.ts[b * kTsPerCta + 39] = globaltimer();
+          if (TS(f) && sA == 0 && pubseg == 0) TS(f)[b * kTsPerCta + 39] = globaltimer();
           red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
-          if (f.ts && sA == 0 && pubseg == 0) f.ts[b * kTsPerCta + 40] = globaltimer();
+          if (TS(f) && sA == 0 && pubseg == 0) TS(f)[b * kTsPerCta + 40] = globaltimer();
         }
-      if (f.ts && first && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 2] = globaltimer();
+      if (TS(f) && first && cw == 0 && lane == 0) TS(f)[b * kTsPerCta + 2] = globaltimer();
       first = false;
       float2 g = make_float2(0.f, 0.f), u = make_float2(0.f, 0.f);
 #pragma unroll 4
@@ -892,13 +986,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         const float gg = pp[0] + pp[2];    // fixed order: half 0 + half 1
         const float uu = pp[1] + pp[3];
         hcur[(long long)r * ffr + h_plane_index(j, ffr)] = gg / (1.0f + expf(-gg)) * uu;
+        // this stage's last phase-A row (known once the producer issued its last one): publish
+        // every segment now instead of at the next item (end marker or W2 rows)
+        if (ti + NS >= slastA)
+          for (const int nseg = snseg; pubseg < nseg; ++pubseg) red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
       }
     }
     if (half == 0 && lane == 0)            // the rest of this stage's segments
       for (const int nseg = snseg; pubseg < nseg; ++pubseg) {
-        if (f.ts && sA == 0) f.ts[b * kTsPerCta + 41 + 2 * pubseg] = globaltimer();
+        if (TS(f) && sA == 0) TS(f)[b * kTsPerCta + 41 + 2 * pubseg] = globaltimer();
         red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
-        if (f.ts && sA == 0) f.ts[b * kTsPerCta + 42 + 2 * pubseg] = globaltimer();
+        if (TS(f) && sA == 0) TS(f)[b * kTsPerCta + 42 + 2 * pubseg] = globaltimer();
       }
     named_bar_sync(2 + sA, 64);
     if (lane == 0) mbar_arrive_cnt(empty + sA, 2);  // release the end marker's stage (both halves)
@@ -907,7 +1005,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       mbar_arrive(pairbar + (sA >> 1));    // (release; merged phase B starts without a CTA barrier)
     }
   }
-  if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 3] = globaltimer();
+  if (TS(f) && cw == 0 && lane == 0) TS(f)[b * kTsPerCta + 3] = globaltimer();
   // h_r -> shared memory (xh) before phase-B segment r: every consumer is done with xh,
   // every stage of every CTA has published its rows of h_r (acquire), then ONE bulk copy
   // (the async proxy reads global memory written through the generic proxy by other CTAs:
@@ -918,8 +1016,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     named_bar_sync(1, nthr);
     if (cw == 0 && lane == 0) {
       const unsigned long long* bar = f.bar + 16 * r;
-      const bool dbg = f.ts && f.ts[b * kTsPerCta + 16] == 0;
-      if (dbg) f.ts[b * kTsPerCta + 16] = globaltimer();  // first h load: CTA out of phase A
+      const bool dbg = TS(f) && TS(f)[b * kTsPerCta + 16] == 0;
+      if (dbg) TS(f)[b * kTsPerCta + 16] = globaltimer();  // first h load: CTA out of phase A
       if (ld_acquire_u64(bar) < bar_target) {
         const unsigned long long t0 = globaltimer();
         while (ld_acquire_u64(bar) < bar_target) {
@@ -927,7 +1025,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();
         }
       }
-      if (dbg) f.ts[b * kTsPerCta + 17] = globaltimer();  // first h published grid-wide
+      if (dbg) TS(f)[b * kTsPerCta + 17] = globaltimer();  // first h published grid-wide
       if (first_h) mbar_wait(&ybar, 0);    // y zeroed by every CTA (acquired by the router warp)
       asm volatile("fence.proxy.async.global;" ::: "memory");
       mbar_arrive_expect_tx(hbar, (uint32_t)ffr * 4u);
@@ -963,13 +1061,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         load_h(sorder[si], si == 0);
         if (si == 0 && active) ph = parB[u];  // written before load_h's barrier
       }
-      if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + (si == 0 ? 4 : 6)] = globaltimer();
+      if (TS(f) && cw == 0 && lane == 0) TS(f)[b * kTsPerCta + (si == 0 ? 4 : 6)] = globaltimer();
       if (!active) continue;
       while (true) {
         mbar_wait(full + s, ph);
         ph ^= 1;
         const int m = meta[s];
-        if (f.ts && cw == 0 && lane == 0 && !f.ts[b * kTsPerCta + 15]) f.ts[b * kTsPerCta + 15] = globaltimer();
+        if (TS(f) && cw == 0 && lane == 0 && !TS(f)[b * kTsPerCta + 15]) TS(f)[b * kTsPerCta + 15] = globaltimer();
         if (m < 0) {                       // kSegB (next expert) or kEnd
           named_bar_sync(bid, 128);
           if (q == 0 && lane == 0) mbar_arrive_cnt(empty + s, kEmptyArrivals);
@@ -980,12 +1078,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         if ((mm || (f.xsep && si == 0)) && !((seen >> r) & 1u)) {  // h_r copied in by the router warp
           mbar_wait(hbarK + r, 0);
           seen |= 1u << r;
-          if (f.ts && cw == 0 && lane == 0 && r == sorder[1 % nseg]) f.ts[b * kTsPerCta + 22] = globaltimer();
+          if (TS(f) && cw == 0 && lane == 0 && r == sorder[1 % nseg]) TS(f)[b * kTsPerCta + 22] = globaltimer();
         }
         // h_r[8k .. 8k+3] / h_r[8k+4 .. 8k+7] (2-plane layout)
         const float4* hp0 = reinterpret_cast<const float4*>(xh + (mm ? f.hoff + (size_t)r * f.hstride : hbo));
         const float4* hp1 = hp0 + (ffr >> 3);
         const int nr = metaN[s];           // rows c .. c+nr-1, contiguous in the stage
+        if (q == 0 && lane == 0) record_event(f, &evn, b, (unsigned)(nr * rowB), 2u + (unsigned)r);
         // partials double-buffered by chunk parity: the next chunk's writes go to the other
         // buffer, so every write-after-read is ordered by a named barrier
         volatile float* pb = partB + (u * 2 + (nchunk++ & 1)) * RBp * 4;
@@ -1000,7 +1099,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         __syncwarp();
         if (lane == 0) mbar_arrive_cnt(empty + s, 1);  // this quarter's reads of the stage are done
         named_bar_sync(bid, 128);          // the 4 quarters of these rows are done
-        if (f.ts && cw == 0 && lane == 0) f.ts[b * kTsPerCta + 23] = globaltimer();  // (last: final B chunk)
+        if (TS(f) && cw == 0 && lane == 0) TS(f)[b * kTsPerCta + 23] = globaltimer();  // (last: final B chunk)
         if (q == 0) {                      // lane i combines row i in a fixed order
           float o = 0.f;
           if (lane < nr) o = ((pb[4 * lane] + pb[4 * lane + 1]) + pb[4 * lane + 2]) + pb[4 * lane + 3];
@@ -1048,11 +1147,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       f.donef[b] = f.donetag;
     }
   }
-  if (f.ts && cw == 0 && lane == 0) {
-    f.ts[b * kTsPerCta + 5] = globaltimer();
-    f.ts[b * kTsPerCta + 34] = clock64();
+  if (TS(f) && cw == 0 && lane == 0) {
+    TS(f)[b * kTsPerCta + 45] = (unsigned long long)evn;  // (this warp's count; the tool trims by time)
+    TS(f)[b * kTsPerCta + 5] = globaltimer();
+    TS(f)[b * kTsPerCta + 34] = clock64();
   }
-  if (f.sts && cw == 0 && lane == 0) f.sts[kStsHead + G + b] = globaltimer();
+  if (STS(f) && cw == 0 && lane == 0) STS(f)[kStsHead + G + b] = globaltimer();
 }
 
 }  // namespace
@@ -1131,6 +1231,11 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   p->pfA = 0;
   p->pfB = p->RB >= 2 ? 1 : 0;
   p->start_rows = -1;  // (runtime default by the number of ways)
+  // interleaved A/B: issuing the next segment's first claim early was neutral to slightly
+  // slower (off); end-of-A markers placed per super-stage before its first W2 rows: Phi -0.5
+  // us, 8x22B P = 8 -0.3, Mixtral -0.3 (on)
+  p->claim_ahead = 0;
+  p->lazy_marks = 1;
   p->pfx = 1;
   p->hoff = hoff;
   p->hstride = hstride;

@@ -94,6 +94,7 @@ struct ExpertArgs {
 };
 
 // Fused persistent expert kernel (expert_fused.cu).
+constexpr int kEvPerCta = 512;  // debug stage events per CTA and call
 constexpr int kFusedMaxDynSmem = 232448 - 1024;  // 227 KB opt-in minus static shared memory
 struct FusedArgs {
   RouteArgs r;                    // routing inputs (every CTA takes the decision; CTA 0 writes it)
@@ -119,9 +120,12 @@ struct FusedArgs {
   int cur_ways, start_rows;       //   first start_rows W1/W3 row pairs of its static block of every
                                   //   way of THIS call's set (slots from cur_pool)
   int pfx;                        // 1: x prefetched into L2 before the PDL wait
+  int claim_ahead;                // 1: a segment's first work claim issued near the end of the previous one
+  int lazy_marks;                 // 1: end-of-A markers placed per super-stage right before its first W2 rows
   int hoff, hstride;              // merged: h_r at xh + hoff + r * hstride
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
+  unsigned long long* ev;         // per-CTA stage events [grid][kEvPerCta][2] {time, bytes} (MOE_DEBUG_TS=1)
   unsigned long long* sts;        // this call's step record [kStsHead + 2*grid] (MOE_DEBUG_TS=1) or nullptr
   // fused TP reduction (f3, moe_tp_connect_*): every term of this rank's partial y goes to
   // the ranks' exchange buffers (layout below); the epilogue sums them into yout
@@ -148,7 +152,7 @@ constexpr int kTpSlotOff = 256;
 inline long long tp_xchg_bytes(int P, int K, int d) { return kTpSlotOff + 2ll * P * K * d * 8; }
 struct FusedPlan {
   int SB, NS, xh_bytes, threads, pctA, pctB, RB, merge, prefetchB, next_rows, pfA, pfB, hoff, hstride;
-  int start_rows, pfx, xsep;
+  int start_rows, pfx, xsep, claim_ahead, lazy_marks;
   size_t smem;
 };
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);

@@ -243,6 +243,7 @@ struct moe_ctx {
   unsigned* h_dbg = nullptr;  // host-mapped kernel progress words (MOE_DEBUG_KERNEL=1)
   unsigned* d_dbg = nullptr;
   unsigned long long* d_ts = nullptr;  // per-CTA phase timestamps (MOE_DEBUG_TS=1)
+  unsigned long long* d_ev = nullptr;  // per-CTA stage events (MOE_DEBUG_TS=1)
   bool coop = false;                   // cooperative launch of the fused kernel (MOE_COOP=1)
   unsigned long long* d_sts = nullptr; // per-call step timestamps, ring of kStsRing (MOE_DEBUG_TS=1)
 };
@@ -483,6 +484,16 @@ MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
   return c->fused_grid;
 }
 
+// Debug only (not in moe.h): per-CTA stage events of the last fused launch -> host
+// ([grid][kEvPerCta][2] {globaltimer ns, bytes | phase << 32}; phase 0/1 = A of segment 0/1,
+// 2 + r = B of routing rank r). Entries of earlier calls may remain: filter by time.
+MOE_API int moe_debug_events(moe_ctx* c, unsigned long long* out) {
+  if (!c || !c->d_ev) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, c->d_ev, sizeof(unsigned long long) * 2 * kEvPerCta * c->fused_grid, cudaMemcpyDeviceToHost);
+  return kEvPerCta;
+}
+
 // Debug only (not in moe.h): the per-call step timestamps (globaltimer ns) of the last
 // kStsRing calls, [kStsRing][kStsHead + 2*grid] = router marks (after its PDL wait, publish,
 // gate GEMV done, softmax done, before the release fence), expert CTA starts, expert CTA ends; slot = seq % kStsRing. Returns the record stride or 0.
@@ -677,6 +688,10 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       const char* pfx = getenv("MOE_PREFETCH_X");      // x into L2 before the PDL wait
       if (pfx) c->plan.pfx = pfx[0] == '1';
       c->plan_RBp = c->plan.RB;                   // (before MOE_ROWS_B)
+      const char* ca = getenv("MOE_CLAIM_AHEAD");  // next segment's first claim issued early
+      if (ca) c->plan.claim_ahead = ca[0] == '1';
+      const char* lm = getenv("MOE_LAZY_MARKS");   // end-of-A markers per super-stage, lazily
+      if (lm) c->plan.lazy_marks = lm[0] == '1';
       const char* xs = getenv("MOE_XSEP");        // x beside one h buffer (default: when the plan allows)
       if (xs && xs[0] == '0') c->plan.xsep = 0;
       const char* mg = getenv("MOE_MERGE");   // merged phases (default: when the plan allows)
@@ -697,6 +712,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
     if (getenv("MOE_DEBUG_TS")) {      // per-CTA phase timestamps in device memory (cheap)
       INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 48 * c->fused_grid));
       INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 48 * c->fused_grid));
+      INIT_TRY(cudaMalloc(&c->d_ev, sizeof(unsigned long long) * 2 * kEvPerCta * c->fused_grid));
+      INIT_TRY(cudaMemset(c->d_ev, 0, sizeof(unsigned long long) * 2 * kEvPerCta * c->fused_grid));
       INIT_TRY(cudaMalloc(&c->d_sts, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
       INIT_TRY(cudaMemset(c->d_sts, 0, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
     }
@@ -785,6 +802,7 @@ MOE_API moe_status moe_destroy(moe_ctx* c) {
   delete c->host;
   c->host = nullptr;
   cudaFree(c->d_ts);
+  cudaFree(c->d_ev);
   cudaFree(c->d_sts);
   if (c->h_mail) cudaFreeHost(c->h_mail);
   if (c->h_last) cudaFreeHost((void*)c->h_last);
@@ -1012,6 +1030,8 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.RB = c->plan.RB;
     fa.RBp = c->plan_RBp;
     fa.xsep = c->plan.xsep;
+    fa.claim_ahead = c->plan.claim_ahead;
+    fa.lazy_marks = c->plan.lazy_marks;
     fa.merge = c->plan.merge;
     fa.prefetchB = c->plan.prefetchB;
     fa.pfA = c->plan.pfA;
@@ -1041,6 +1061,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.hstride = c->plan.hstride;
     fa.dbg = c->d_dbg;
     fa.ts = c->d_ts;
+    fa.ev = c->d_ev;
     fa.sts = ra.sts;
     fa.tpP = tpf ? c->P : ll1 ? 1 : 0;
     fa.tp_rank = tpf ? c->rank : 0;

@@ -7,7 +7,7 @@ each mark, the median / min / max over CTAs relative to the END of the previous 
 (the latest CTA end of call seq-1, from moe_debug_step_ts): what the one-kernel step
 spends between the previous step's last byte and this step's first / last byte.
 
-    MOE_DEBUG_TS=1 python tools/timeline.py --shape mixtral-8x7b
+    python tools/timeline.py --shape mixtral-8x7b    (loads lib/libmoe_debug.so)
 """
 from __future__ import annotations
 
@@ -21,6 +21,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("MOE_DEBUG_TS", "1")
+# the marks exist only in the debug build of the library
+os.environ.setdefault("MOE_LIB_PATH", os.path.join(ROOT, "paper_2512_16473_b200", "lib", "libmoe_debug.so"))
 
 import numpy as np  # noqa: E402
 
@@ -36,7 +38,7 @@ MARKS = {0: "cta_start", 8: "pdl_wait_done", 9: "x_landed", 10: "router_has_logi
          19: "merged_h0_published", 20: "merged_h1_published", 22: "merged_h1_landed_warp0",
          23: "warp0_last_B_chunk_done", 38: "prod_first_row_issued", 39: "st0_pub_h0_before", 40: "st0_pub_h0_after",
          41: "st0_end_pub_seg0_before", 42: "st0_end_pub_seg0_after", 43: "st0_end_pub_seg1_before",
-         44: "st0_end_pub_seg1_after"}
+         44: "st0_end_pub_seg1_after", 46: "router_h1_copy_landed", 47: "router_h1_settled"}
 KSTS_RING, KSTS_HEAD = 64, 8
 
 
@@ -67,6 +69,9 @@ def main():
         stride = KSTS_HEAD + 2 * G
         sts = np.zeros(KSTS_RING * stride, np.uint64)
         lib.moe_debug_step_ts(m._h.value, sts.ctypes.data)
+        lib.moe_debug_events.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        ev = np.zeros(G * 512 * 2, np.uint64)
+        lib.moe_debug_events(m._h.value, ev.ctypes.data)
     ts = ts.reshape(G, 48).astype(np.int64)
     sts = sts.reshape(KSTS_RING, stride).astype(np.int64)
     last = args.steps  # seq of the last call (seqs start at 1)
@@ -109,6 +114,25 @@ def main():
     if ok.any():
         mhz = (ts[ok, 34] - ts[ok, 33]) / ((ts[ok, 5] - ts[ok, 0]) / 1e3)
         out["sm_mhz_effective"] = {"median": float(np.median(mhz)), "min": float(mhz.min()), "max": float(mhz.max())}
+    # stage-data arrival curve: bytes the consumers took per 0.5 us bin (upper bound on the
+    # landing time: a consumer still busy sees its stage later), from the per-CTA events
+    ev = ev.reshape(G * 512, 2).astype(np.int64)
+    t = ev[:, 0] - prev_end
+    ok = (ev[:, 0] > prev_end) & (ev[:, 0] <= cur_end)
+    if ok.any():
+        tb = t[ok]
+        by = ev[ok, 1] & 0xffffffff
+        ph = ev[ok, 1] >> 32
+        binw = 500
+        nb = int(tb.max() // binw) + 1
+        curve = []
+        for k in range(nb):
+            sel = (tb >= k * binw) & (tb < (k + 1) * binw)
+            curve.append(round(float(by[sel].sum()) / binw / 1e3, 2))  # TB/s (bytes/ns / 1e3)
+        out["arrival_TBs_per_0.5us"] = curve
+        out["phase_bytes_first_last_us"] = {int(p): [round(float(tb[ph == p].min()) / 1e3, 2),
+                                                    round(float(tb[ph == p].max()) / 1e3, 2),
+                                                    int(by[ph == p].sum())] for p in np.unique(ph)}
     print(json.dumps(out, indent=1))
 
 
