@@ -164,6 +164,16 @@ __device__ __forceinline__ float ld_relaxed_f32(const float* p) {
 // h words [0, n) of a shared-memory copy (thread t of nt): re-read every still-armed word from
 // `src` (L2) until it is written. Loads are batched 8 float4 deep with one branch per batch
 // (one load-compare-branch chain per float4 made the router warp's scan of Phi's h 5 us).
+// debug build only (MOE_DEBUG_STALE_H=1, a fault injection for the tests): before settling,
+// re-arm one word of every float4 this thread checks in the shared-memory copy, as if its
+// store had not reached L2 when the copy read it; the settle must fetch every one again
+__device__ __forceinline__ void inject_stale_h(const FusedArgs& f, float* dst, int n, int t, int nt) {
+#ifdef MOE_DEBUG_MARKS
+  if (!f.dbg_stale) return;
+  for (int i = 4 * t, k = 0; i < n; i += 4 * nt, ++k) dst[i + (k & 3)] = __uint_as_float(kHUnset);
+#endif
+}
+
 __device__ __noinline__ void settle_h(float* dst, const float* src, int n, int t, int nt) {
   constexpr int U = 8;
   for (int base = 4 * t; base < n; base += 4 * nt * U) {
@@ -710,6 +720,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         }
         mbar_wait(hrawK + r, 0);
         if (TS(f) && lane == 0 && si == 1) TS(f)[b * kTsPerCta + 46] = globaltimer();  // h1 bulk copy landed
+        inject_stale_h(f, hs, ffr, lane, 32);
         settle_h(hs, hg, ffr, lane, 32);   // words whose store had not reached L2 yet
         if (TS(f) && lane == 0 && si == 1) TS(f)[b * kTsPerCta + 47] = globaltimer();  // h1 settled
         mbar_arrive(hbarK + r);            // (count 32: each lane after its own settled words)
@@ -1033,6 +1044,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
     mbar_wait(hbar, hph);
     hph ^= 1;
+    inject_stale_h(f, reinterpret_cast<float*>(xh + hbo), ffr, ctid, nthr);
     settle_h(reinterpret_cast<float*>(xh + hbo), hcur + (long long)r * ffr, ffr, ctid, nthr);
     named_bar_sync(1, nthr);               // every settled word visible to every consumer
   };

@@ -124,6 +124,7 @@ struct FusedArgs {
   int lazy_marks;                 // 1: end-of-A markers placed per super-stage right before its first W2 rows
   int hoff, hstride;              // merged: h_r at xh + hoff + r * hstride
   unsigned* dbg;                  // host-mapped progress counters (MOE_DEBUG_KERNEL=1) or nullptr
+  int dbg_stale;                  // debug build: MOE_DEBUG_STALE_H=1 re-arms h words before the settle
   unsigned long long* ts;         // per-CTA phase timestamps [grid][8] (MOE_DEBUG_TS=1) or nullptr
   unsigned long long* ev;         // per-CTA stage events [grid][kEvPerCta][2] {time, bytes} (MOE_DEBUG_TS=1)
   unsigned long long* sts;        // this call's step record [kStsHead + 2*grid] (MOE_DEBUG_TS=1) or nullptr

@@ -158,7 +158,8 @@ struct moe_ctx {
   RouteRec* d_route = nullptr;
   float* d_h = nullptr;
   float* d_hf = nullptr;
-  int plan_RBp = 0;                    // phase-B partials row stride (plan's RB before MOE_ROWS_B)               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
+  int plan_RBp = 0;                    // phase-B partials row stride (plan's RB before MOE_ROWS_B)
+  int dbg_stale = 0;                   // MOE_DEBUG_STALE_H=1 (debug build): settle fault injection               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
   moe_access_record* d_trace = nullptr;
   long long trace_cap = 0, trace_count = 0;
   std::vector<uint32_t> tokens;  // per-layer call count = token index
@@ -699,6 +700,7 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       const char* rb = getenv("MOE_ROWS_B");  // W2 rows per phase-B super-stage (<= plan's)
       if (rb && atoi(rb) >= 1 && atoi(rb) < c->plan.RB) c->plan.RB = atoi(rb);
     }
+    c->dbg_stale = getenv("MOE_DEBUG_STALE_H") != nullptr;
     if (getenv("MOE_STREAM_TIMELINE")) {
       c->tl = true;
       INIT_TRY(cudaEventCreate(&c->tl_base));
@@ -718,8 +720,9 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       INIT_TRY(cudaMemset(c->d_sts, 0, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));
     }
     if (getenv("MOE_DEBUG_KERNEL") || getenv("MOE_DEBUG_TS")) {
-      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d RB=%d merge=%d xh=%d smem=%zu grid=%d\n", (int)c->fused,
-              c->plan.NS, c->plan.SB, c->plan.RB, c->plan.merge, c->plan.xh_bytes, c->plan.smem, c->fused_grid);
+      fprintf(stderr, "[moe init] fused=%d NS=%d SB=%d RB=%d merge=%d xsep=%d xh=%d smem=%zu grid=%d\n", (int)c->fused,
+              c->plan.NS, c->plan.SB, c->plan.RB, c->plan.merge, c->plan.xsep, c->plan.xh_bytes, c->plan.smem,
+              c->fused_grid);
   }
   }
   {
@@ -1060,6 +1063,7 @@ static moe_status forward_impl(moe_ctx* c, int32_t layer, const void* x, float* 
     fa.hoff = c->plan.hoff;
     fa.hstride = c->plan.hstride;
     fa.dbg = c->d_dbg;
+    fa.dbg_stale = c->dbg_stale;
     fa.ts = c->d_ts;
     fa.ev = c->d_ev;
     fa.sts = ra.sts;
