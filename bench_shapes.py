@@ -39,6 +39,7 @@ SHAPES = {
     "8x22b-P2": (6144, 8192, 8, 2),
     "8x22b-P4": (6144, 4096, 8, 2),
     "8x22b-P8": (6144, 2048, 8, 2),
+    "mixtral-8x7b-P8": (4096, 1792, 8, 2),   # configs[1]'s layer split 8 ways: one rank's work
 }
 
 

@@ -823,9 +823,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       // go into a super-stage's two stages right before its first W2 rows, starting with the
       // super-stage whose stages drain first (the ring's next stages in issue order): W2 rows
       // enter as soon as one super-stage is free instead of after the whole ring drained.
-      int tb = f.lazy_marks ? ((t % NS) + 1) / 2 : 0;
-      uint32_t marked = 0u;
       const int t_a = t;                              // phase-A items issued by this CTA
+      // (only with a full ring of phase-A items: a CTA with a few rows — the tiny shapes —
+      // publishes its h rows sooner with every end marker placed at once, +1.5 us otherwise)
+      const bool lazy = f.lazy_marks && t_a >= NS;
+      int tb = lazy ? ((t % NS) + 1) / 2 : 0;
+      uint32_t marked = 0u;
       auto mark_end_a = [&](int u) {
         if ((marked >> u) & 1u) return;
         marked |= 1u << u;
@@ -845,10 +848,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           mbar_arrive(full + s);
         }
       };
-      if (f.lazy_marks)                               // super-stages that got no phase-A item: at once
+      if (lazy)                                       // super-stages that got no phase-A item: at once
         for (int u = 0; u < NSB; ++u)
           if (2 * u >= t_a) mark_end_a(u);
-      if (!f.lazy_marks) {                            // every end-of-A marker first, in drain order
+      if (!lazy) {                                    // every end-of-A marker first, in drain order
         for (int k = 0; k < NS; ++k, ++t) {
           const int s = t % NS;
           acquire(s);
