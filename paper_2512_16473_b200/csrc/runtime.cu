@@ -159,7 +159,9 @@ struct moe_ctx {
   float* d_h = nullptr;
   float* d_hf = nullptr;
   int plan_RBp = 0;                    // phase-B partials row stride (plan's RB before MOE_ROWS_B)
-  int dbg_stale = 0;                   // MOE_DEBUG_STALE_H=1 (debug build): settle fault injection               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
+  int dbg_stale = 0;                   // MOE_DEBUG_STALE_H=1 (debug build): settle fault injection
+  static constexpr size_t kDevPtrCache = 1024;  // forward_host: pinned host -> device pointers
+  const void* dp_host[kDevPtrCache] = {};       // (identity-mapped pointers seen)               // fused kernel: h [2 (call parity)][K][ffr], see expert_fused.cu
   moe_access_record* d_trace = nullptr;
   long long trace_cap = 0, trace_count = 0;
   std::vector<uint32_t> tokens;  // per-layer call count = token index
@@ -1376,11 +1378,25 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint1
   // writes y straight into it — no copy-engine transfer queued in front of or behind it.
   void* xd = nullptr;
   void* yd = nullptr;
-  const bool zc = c->fused && (c->P == 1 || c->tp_fused) &&
-                  cudaHostGetDevicePointer(&xd, (void*)x_host, 0) == cudaSuccess &&
-                  cudaHostGetDevicePointer(&yd, (void*)y_host, 0) == cudaSuccess && c->d % 8 == 0 &&
-                  ((uintptr_t)xd & 15) == 0 && ((uintptr_t)yd & 15) == 0;
-  cudaGetLastError();
+  // host -> device pointer of a pinned buffer: a driver call per pointer the first time, then
+  // from a small direct-mapped cache (decode calls cycle over a few buffers). Only identity
+  // mappings are cached (pinned memory under unified addressing, where the device pointer is
+  // the host pointer whatever allocation later reuses the address); others ask every call.
+  auto devptr = [&](const void* h, void** out) -> bool {
+    const size_t slot = ((uintptr_t)h >> 4) % moe_ctx::kDevPtrCache;
+    if (c->dp_host[slot] == h) {
+      *out = const_cast<void*>(h);
+      return true;
+    }
+    if (cudaHostGetDevicePointer(out, (void*)h, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (*out == h) c->dp_host[slot] = h;
+    return true;
+  };
+  const bool zc = c->fused && (c->P == 1 || c->tp_fused) && devptr(x_host, &xd) && devptr(y_host, &yd) &&
+                  c->d % 8 == 0 && ((uintptr_t)xd & 15) == 0 && ((uintptr_t)yd & 15) == 0;
   if (zc && !c->tp_fused && !c->d_ll1) {
     const long long bytes = tp_xchg_bytes(1, c->K, c->d);
     CUDA_TRY(cudaMalloc(&c->d_ll1, (size_t)bytes));
@@ -1403,13 +1419,18 @@ MOE_API moe_status moe_layer_forward_host(moe_ctx* c, int32_t layer, const uint1
     st = forward_impl(c, layer, c->d_x_e2e, c->d_y_e2e, s, (const uint16_t*)xd, (float*)yd, tag);
     if (st != MOE_OK) return st;
     if (flags) {
-      CUDA_TRY(cudaEventRecord(c->host_ev, s));
       const int G = c->fused_grid;
       const auto t0 = std::chrono::steady_clock::now();
+      bool recorded = false;                 // (the event only for a call that takes > 2 s)
       for (int b = 0; b < G; ++b) {
         while (c->h_done[b] != tag) {
-          // a kernel that failed never writes its flags: fall back to the event's verdict
+          // a kernel that failed never writes its flags: fall back to the event's verdict (an
+          // event recorded now completes after the kernel, or reports its error)
           if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+            if (!recorded) {
+              CUDA_TRY(cudaEventRecord(c->host_ev, s));
+              recorded = true;
+            }
             cudaError_t q = cudaEventQuery(c->host_ev);
             if (q != cudaErrorNotReady && c->h_done[b] != tag) {
               CUDA_TRY(q);
