@@ -539,7 +539,8 @@ def test_fused_path_odd_shapes(L, d, ff, n, K, M, T):
 @pytest.mark.parametrize("env", [{"MOE_EXPERT_PATH": "split"}, {"MOE_COOP": "1"}, {"MOE_PDL": "0"},
                                  {"MOE_STATIC_A": "0", "MOE_STATIC_B": "0"},
                                  {"MOE_STATIC_A": "100", "MOE_STATIC_B": "100"},
-                                 {"MOE_MERGE": "0"}, {"MOE_PREFETCH_B": "0"}, {"MOE_ROWS_B": "1"}])
+                                 {"MOE_MERGE": "0"}, {"MOE_PREFETCH_B": "0"}, {"MOE_ROWS_B": "1"},
+                                 {"MOE_LAZY_MARKS": "0"}, {"MOE_CLAIM_AHEAD": "1"}, {"MOE_PREFETCH_START": "0"}])
 def test_launch_and_schedule_variants(tiny, monkeypatch, env):
     """Every launch / schedule variant the runtime can take gives the same bit-exact trace and
     outputs: the split fallback, the cooperative launch, no PDL, all-stolen and all-static
@@ -562,6 +563,32 @@ def test_launch_and_schedule_variants(tiny, monkeypatch, env):
             m.configure(ways=2, indexes=3)
             y0 = harness.run_decode(m, x)
         assert np.array_equal(y.view(np.uint32), y0.view(np.uint32))
+
+
+@pytest.mark.parametrize("env", [{"MOE_XSEP": "0"}, {"MOE_LAZY_MARKS": "0"}, {"MOE_CLAIM_AHEAD": "1"},
+                                 {"MOE_STATIC_B": "0"}, {"MOE_PREFETCH_START": "0", "MOE_PREFETCH_X": "0"}])
+def test_single_row_chunk_layout_variants(monkeypatch, env):
+    """Single-row W2 chunks (ff_r 14336: a W2 row spans two stages) take the x-beside-h layout
+    (the first expert's phase B without a CTA barrier); the segmented layout (MOE_XSEP=0), all
+    end-of-A markers at once, early work claims, an all-stolen phase B and no L2 warm-up give
+    the same bit-exact trace and the same y bits, on a cold cache with misses."""
+    hm = harness.host_model(1, 1024, 14336, 8, 2)
+    x, ranked = harness.hidden_states(hm, 10, "paper")
+    ref = _oracle_run(hm, x, N=1, M=4)
+
+    def run():
+        with harness.open_moe(hm) as m:
+            assert m.runtime_info()["expert_path"] == "fused"
+            m.configure(ways=4, indexes=1)
+            y = harness.run_decode(m, x)
+            _compare(hm, m, x, ref, y)
+            return y
+
+    y0 = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    y1 = run()
+    assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
 
 
 @pytest.mark.parametrize("mt", ["2", "0"])
