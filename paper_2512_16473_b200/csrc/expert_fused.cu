@@ -1235,7 +1235,9 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   // (bench_shapes.py sweeps): 95% of phase A; 10% of phase B with 1-2-row chunks, 20% with
   // bigger ones (8x22B slices) — phase B's expert switch and the end of the step leave the
   // CTAs unevenly advanced, and a long stolen tail re-balances them
-  p->pctA = 95;
+  // (round 2: with fewer than 32 phase-A rows per CTA and expert — the 8x22B P = 4 / 8 and
+  // Mixtral P = 8 slices — a 10% stolen tail balances better: -0.1-0.3 us; Phi keeps 95)
+  p->pctA = ffr / grid < 32 ? 90 : 95;
   p->pctB = p->RB <= 2 ? 10 : 20;
   p->merge = merge ? 1 : 0;
   p->prefetchB = 1;
