@@ -466,9 +466,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   }
   if (threadIdx.x == 32) ra = f.r;  // kernel parameters -> shared memory before the PDL wait
   __syncthreads();          // mbarrier inits and routing arguments visible
-#ifdef MOE_EARLY_TRIGGER
-  griddep_launch_dependents();
-#endif
   const int nwc = kWarpsPerStage * NS;
   // Programmatic dependent launch: the previous call's kernel (cache directory, counters,
   // h) and the caller's x are complete and visible after this wait.
