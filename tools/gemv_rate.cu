@@ -1,10 +1,11 @@
 // Gate-GEMV arithmetic rates on one SM (the decode kernel's routing prologue): 20 consumer
 // warps, 16 gate rows x 4096 bf16 in shared memory, each thread one 16-B chunk of x and of
-// every row, accumulated into even/odd fp32 lanes in the same order three ways:
+// every row, accumulated into even/odd fp32 lanes in the same order four ways:
 //   0  fma.rn.f32.bf16 (mixed precision, SASS FHFMA.BF16)
 //   1  bf16 -> fp32 by shift/mask, then fma.rn.f32x2 (FFMA2)
 //   2  bf16 -> fp32 by shift/mask, then two FFMA
-// Prints SM cycles per pass (clock64, median CTA) and checks the three give identical bits.
+//   3  a third of the rows as 0, the rest as 1 (fma and alu pipes both busy)
+// Prints SM cycles per pass (clock64, median CTA) and checks the four give identical bits.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gemv_rate tools/gemv_rate.cu
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -45,6 +46,7 @@ __device__ __forceinline__ float2 dot8(const int4 w, const float2 (&xf)[4], cons
       acc.x = fmaf(wf.x, xf[i].x, acc.x);
       acc.y = fmaf(wf.y, xf[i].y, acc.y);
     }
+    if (MODE == 3) acc = ffma2(bf2(ww[i]), xf[i], acc);   // (mode 3 mixes: see the kernel)
   }
   return acc;
 }
@@ -74,7 +76,13 @@ __global__ void __launch_bounds__(640, 1) gemv(const uint16_t* Wg, const uint16_
       if (t < nch) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (e0 + j < n) acc[j] = dot8<MODE>(reinterpret_cast<const int4*>(sm + (size_t)(e0 + j) * gstride)[t], xf, xr, acc[j]);
+          if (e0 + j < n) {
+            const int4 w = reinterpret_cast<const int4*>(sm + (size_t)(e0 + j) * gstride)[t];
+            // mode 3: rows j % 3 == 0 on the mixed-precision FMA (fma pipe only), the others
+            // converted on the ALU pipe and accumulated with packed FFMA2 (half the fma slots)
+            if (MODE == 3) acc[j] = (j % 3 == 0) ? dot8<0>(w, xf, xr, acc[j]) : dot8<3>(w, xf, xr, acc[j]);
+            else acc[j] = dot8<MODE>(w, xf, xr, acc[j]);
+          }
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) res += (acc[j].x + acc[j].y) * (rep == 0 ? 1.f : 0.f);
@@ -98,14 +106,14 @@ int main() {
   long long* dc;
   cudaMalloc(&dw, hw.size() * 2);
   cudaMalloc(&dx, hx.size() * 2);
-  cudaMalloc(&dout, (size_t)G * T * 4 * 3);
+  cudaMalloc(&dout, (size_t)G * T * 4 * 4);
   cudaMalloc(&dc, G * 8);
   cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
   const int smem = n * (2 * d + 16);
-  std::vector<float> outs[3];
-  for (int mode = 0; mode < 3; ++mode) {
-    auto k = mode == 0 ? gemv<0> : mode == 1 ? gemv<1> : gemv<2>;
+  std::vector<float> outs[4];
+  for (int mode = 0; mode < 4; ++mode) {
+    auto k = mode == 0 ? gemv<0> : mode == 1 ? gemv<1> : mode == 2 ? gemv<2> : gemv<3>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k<<<G, T, smem>>>(dw, dx, d, n, dout + (size_t)mode * G * T, dc);
     k<<<G, T, smem>>>(dw, dx, d, n, dout + (size_t)mode * G * T, dc);
@@ -117,7 +125,7 @@ int main() {
     printf("{\"mode\": %d, \"cycles_per_gemv_median\": %lld, \"err\": \"%s\"}\n", mode, c[G / 2],
            cudaGetErrorString(cudaGetLastError()));
   }
-  const bool same = outs[0] == outs[1] && outs[0] == outs[2];
+  const bool same = outs[0] == outs[1] && outs[0] == outs[2] && outs[0] == outs[3];
   printf("{\"bit_identical\": %s}\n", same ? "true" : "false");
   return 0;
 }
