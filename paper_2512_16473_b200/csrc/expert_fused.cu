@@ -1070,7 +1070,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           ph = parB[u];
         }
       } else {
-        load_h(sorder[si], si == 0);
+        // (xsep: a super-stage that got no chunk of the first expert never waited for its h —
+        // and with it for the y counter — so the reload acquires the y zeroing here too)
+        load_h(sorder[si], si == 0 || f.xsep);
         if (si == 0 && active) ph = parB[u];  // written before load_h's barrier
       }
       if (TS(f) && cw == 0 && lane == 0) TS(f)[b * kTsPerCta + (si == 0 ? 4 : 6)] = globaltimer();

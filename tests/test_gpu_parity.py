@@ -591,6 +591,29 @@ def test_single_row_chunk_layout_variants(monkeypatch, env):
     assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
 
 
+def test_single_row_chunk_layout_few_rows_per_cta(monkeypatch):
+    """x beside one h buffer with d = 64: most CTAs get no W2 row of the first expert, so
+    their super-stages reach the second expert's h reload without having waited for the first
+    expert's h (nor, through it, for every CTA's y zeroing): the reload acquires it itself.
+    Bit-exact traces, y within the bar, and the same bits as the segmented layout."""
+    hm = harness.host_model(1, 64, 14336, 8, 2)
+    x, ranked = harness.hidden_states(hm, 16, "paper")
+    ref = _oracle_run(hm, x, N=1, M=8, warm=True)
+
+    def run():
+        with harness.open_moe(hm) as m:
+            assert m.runtime_info()["expert_path"] == "fused"
+            m.configure(ways=8, indexes=1, warm_start=True)
+            y = harness.run_decode(m, x)
+            _compare(hm, m, x, ref, y)
+            return y
+
+    y0 = run()
+    monkeypatch.setenv("MOE_XSEP", "0")
+    y1 = run()
+    assert np.array_equal(y0.view(np.uint32), y1.view(np.uint32))
+
+
 @pytest.mark.parametrize("mt", ["2", "0"])
 @pytest.mark.parametrize("T", [100, 300, 700])
 def test_prefill_pair_kernel_small_shape(monkeypatch, mt, T):
