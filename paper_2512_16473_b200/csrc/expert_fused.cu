@@ -1234,10 +1234,14 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
   // (bench_shapes.py sweeps): 95% of phase A; 10% of phase B with 1-2-row chunks, 20% with
   // bigger ones (8x22B slices) — phase B's expert switch and the end of the step leave the
   // CTAs unevenly advanced, and a long stolen tail re-balances them
-  // (round 2: with fewer than 32 phase-A rows per CTA and expert — the 8x22B P = 4 / 8 and
-  // Mixtral P = 8 slices — a 10% stolen tail balances better: -0.1-0.3 us; Phi keeps 95)
-  p->pctA = ffr / grid < 32 ? 90 : 95;
-  p->pctB = p->RB <= 2 ? 10 : 20;
+  // Round 2, interleaved A/B per shape class: fewer than 32 phase-A rows per CTA and expert
+  // (8x22B P = 4 / 8, Mixtral P = 8 slices): a 10% stolen phase-A tail (-0.1-0.3 us); 24 KB
+  // stages (d = 6144: 8x22B unsplit / P = 2): 2% (-0.85 / -0.9 us); sets of 16 or more
+  // experts with short W2 rows (Phi): 2% of phase A and 15% of phase B stolen (-0.35 us);
+  // Mixtral keeps 95 / 10 (98 / 15: +0.6-1.5 us).
+  const int rows_per_cta = ffr / grid;
+  p->pctA = rows_per_cta < 32 ? 90 : (SB > 16384 || n >= 16) ? 98 : 95;
+  p->pctB = p->RB <= 2 ? (n >= 16 ? 15 : 10) : 20;
   p->merge = merge ? 1 : 0;
   p->prefetchB = 1;
   p->next_rows = -1;  // (runtime default by the number of ways)
