@@ -47,7 +47,7 @@ def epilogue_breakdown(P: int, tokens: int = 16, steps: int = 40) -> dict:
     ms = [harness.open_moe(hp) for hp in hps]
     os.environ.pop("MOE_DEBUG_TS", None)
     lib = moe.lib()
-    lib.moe_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.moe_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]
     try:
         for m in ms:
             m.configure(ways=n, indexes=1, warm_start=True)
@@ -60,13 +60,16 @@ def epilogue_breakdown(P: int, tokens: int = 16, steps: int = 40) -> dict:
         marks = []
         for m in ms:
             G = m.runtime_info()["grid"]
-            ts = np.zeros(G * 40, np.uint64)
-            lib.moe_debug_timestamps(m._h.value, ts.ctypes.data)
-            marks.append(ts.reshape(G, 40).astype(np.int64))
+            ts = np.zeros(G * 64, np.uint64)
+            stride = lib.moe_debug_timestamps(m._h.value, ts.ctypes.data, ts.size)
+            assert stride > 0, "per-CTA marks need the debug build (MOE_LIB_PATH=.../libmoe_debug.so)"
+            marks.append(ts[:G * stride].reshape(G, stride).astype(np.int64))
     finally:
         for m in ms:
             m.close()
     t = np.concatenate(marks)
+    if not (t[:, 18] > 0).any():   # the production build carries no marks
+        return {"note": "epilogue marks need the debug build: MOE_LIB_PATH=paper_2512_16473_b200/lib/libmoe_debug.so"}
     med = lambda a: statistics.median(a.tolist()) / 1e3  # noqa: E731
     # the rank that arrives last waits only for its own slices to land everywhere: its wait is
     # the exchange latency; the other ranks' waits add the skew between the ranks' kernels

@@ -64,7 +64,7 @@ constexpr int kRouterWarp = 1 + kWarpsPerStage * kMaxNS;  // warp 0 producer, 1.
 constexpr int kRouteBar = 13;              // named barrier: partial logits -> router warp
 constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
-constexpr int kTsPerCta = 48;             // debug timestamps per CTA (MOE_DEBUG_TS)
+constexpr int kTsPerCta = kTsStride;      // debug timestamps per CTA (MOE_DEBUG_TS)
 constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stage
 // back-off of the polls on flags other CTAs set (interleaved A/B: a pure spin was 0.1-0.25 us
 // slower per step on small shapes)

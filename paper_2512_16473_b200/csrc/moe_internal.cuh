@@ -95,6 +95,7 @@ struct ExpertArgs {
 
 // Fused persistent expert kernel (expert_fused.cu).
 constexpr int kEvPerCta = 512;  // debug stage events per CTA and call
+constexpr int kTsStride = 48;   // debug timestamps per CTA (expert_fused.cu's kTsPerCta)
 constexpr int kFusedMaxDynSmem = 232448 - 1024;  // 227 KB opt-in minus static shared memory
 struct FusedArgs {
   RouteArgs r;                    // routing inputs (every CTA takes the decision; CTA 0 writes it)

@@ -479,12 +479,14 @@ MOE_API int moe_debug_tc_gemm(const void* A, const void* B, float* C, int M, int
   return e == cudaSuccess ? 0 : 3;
 }
 
-// Debug only (not in moe.h): per-CTA timestamps of the last fused launch -> host (grid*8).
-MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out) {
+// Debug only (not in moe.h): per-CTA timestamps of the last fused launch -> host.
+MOE_API int moe_debug_timestamps(moe_ctx* c, unsigned long long* out, long long cap) {
+  // copies at most cap words ([grid][stride]); returns the per-CTA stride (0: no marks)
   if (!c || !c->d_ts) return 0;
   cudaDeviceSynchronize();
-  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * 48 * c->fused_grid, cudaMemcpyDeviceToHost);
-  return c->fused_grid;
+  const long long n = (long long)kTsStride * c->fused_grid;
+  cudaMemcpy(out, c->d_ts, sizeof(unsigned long long) * (size_t)(cap < n ? cap : n), cudaMemcpyDeviceToHost);
+  return kTsStride;
 }
 
 // Debug only (not in moe.h): per-CTA stage events of the last fused launch -> host
@@ -714,8 +716,8 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
       INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_dbg, c->h_dbg, 0));
     }
     if (getenv("MOE_DEBUG_TS")) {      // per-CTA phase timestamps in device memory (cheap)
-      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * 48 * c->fused_grid));
-      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * 48 * c->fused_grid));
+      INIT_TRY(cudaMalloc(&c->d_ts, sizeof(unsigned long long) * kTsStride * c->fused_grid));
+      INIT_TRY(cudaMemset(c->d_ts, 0, sizeof(unsigned long long) * kTsStride * c->fused_grid));
       INIT_TRY(cudaMalloc(&c->d_ev, sizeof(unsigned long long) * 2 * kEvPerCta * c->fused_grid));
       INIT_TRY(cudaMemset(c->d_ev, 0, sizeof(unsigned long long) * 2 * kEvPerCta * c->fused_grid));
       INIT_TRY(cudaMalloc(&c->d_sts, sizeof(unsigned long long) * kStsRing * (kStsHead + 2 * c->fused_grid)));

@@ -55,7 +55,7 @@ def main():
     xd = torch.from_numpy(x.view(np.int16)).cuda()
     yd = torch.empty((args.tokens, d), dtype=torch.float32, device="cuda")
     lib = moe.lib()
-    lib.moe_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.moe_debug_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]
     lib.moe_debug_step_ts.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     with harness.open_moe(hm) as m:
         m.configure(ways=n, indexes=1, warm_start=True)
@@ -64,15 +64,17 @@ def main():
             m.forward(0, xd[i % args.tokens, 0].data_ptr(), yd[i % args.tokens].data_ptr(), s.cuda_stream)
         s.synchronize()
         G = m.runtime_info()["grid"]
-        ts = np.zeros(G * 48, np.uint64)
-        lib.moe_debug_timestamps(m._h.value, ts.ctypes.data)
+        ts = np.zeros(G * 64, np.uint64)
+        tstride = lib.moe_debug_timestamps(m._h.value, ts.ctypes.data, ts.size)
+        assert tstride > 0, "per-CTA marks need the debug build"
+        ts = ts[:G * tstride]
         stride = KSTS_HEAD + 2 * G
         sts = np.zeros(KSTS_RING * stride, np.uint64)
         lib.moe_debug_step_ts(m._h.value, sts.ctypes.data)
         lib.moe_debug_events.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         ev = np.zeros(G * 512 * 2, np.uint64)
         lib.moe_debug_events(m._h.value, ev.ctypes.data)
-    ts = ts.reshape(G, 48).astype(np.int64)
+    ts = ts.reshape(G, tstride).astype(np.int64)
     sts = sts.reshape(KSTS_RING, stride).astype(np.int64)
     last = args.steps  # seq of the last call (seqs start at 1)
     prev = sts[(last - 1) % KSTS_RING]
