@@ -1210,8 +1210,12 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
     if (ns > kMaxNS) ns = kMaxNS;
     return ns & ~1;                              // stages pair into super-stages in phase B
   };
-  // merged phase B when holding every expert's h costs no ring stage (small ff_r)
-  const bool merge = K == kMaxFusedK && stages(xh2) == stages(xh1);
+  // merged phase B when holding every expert's h costs no ring stage (small ff_r) ...
+  // ... and also where it costs ring stages, as long as the smaller ring still holds 144 KB
+  // in flight per SM (interleaved A/B: 8x22B P = 4 slice, 8 -> 6 stages of 24 KB: -2.7 us;
+  // Mixtral, 10 -> 6 stages of 16 KB: +2.6 us)
+  const bool merge = K == kMaxFusedK &&
+                     (stages(xh2) == stages(xh1) || (stages(xh2) >= 4 && (long long)stages(xh2) * SB >= 144 * 1024));
   // otherwise x and ONE h buffer side by side when that costs no ring stage either: phase B of
   // the first expert then starts per super-stage as in the merged mode (xsep)
   const int xh3 = hoff + hstride;
