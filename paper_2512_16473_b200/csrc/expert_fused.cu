@@ -240,12 +240,18 @@ __device__ __forceinline__ void tp_push(const FusedArgs& f, int r, int c, float 
   const unsigned long long w = tp_tag(f) | __float_as_uint(v);
   for (int p = 0; p < f.tpP; ++p) st_relaxed_sys_u64(tp_slot(f, p, f.tp_rank, r, c), w);
 }
-__device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, int G, int ctid, int nthr) {
-  const int P = f.tpP, K = f.e.K, d = f.e.d, PK = P * K;  // PK in {1, 2, 4, 8, 16}: divides 32 and nthr
+// (out of line with scalar arguments: a single-GPU step never runs it; it reads only this
+// rank's own exchange buffer `own`)
+__device__ __noinline__ void tp_reduce_epilogue(uint8_t* own, int P, int K, int d, unsigned long long tp_calls,
+                                                float* yout, unsigned long long* ts, int b, int G, int ctid,
+                                                int nthr) {
+  const int PK = P * K;  // PK in {1, 2, 4, 8, 16}: divides 32 and nthr
   const int c0 = (int)((long long)d * b / G), c1 = (int)((long long)d * (b + 1) / G);
   const int total = (c1 - c0) * PK;
-  const unsigned long long tag = tp_tag(f);
-  unsigned long long* ts = TS(f) ? TS(f) + b * kTsPerCta : nullptr;  // debug marks 18, 21
+  const unsigned long long tag = (unsigned long long)(uint32_t)(tp_calls + 1) << 32;  // (tp_tag)
+  const int par = (int)(tp_calls & 1);
+  // [parity][column][source rank][routing rank] (tp_slot): the P*K words of a column are contiguous
+  const unsigned long long* slots = reinterpret_cast<const unsigned long long*>(own + kTpSlotOff) + (long long)par * d * PK;
   if (ts && ctid == 0) ts[18] = globaltimer();
   // thread i holds word j = i % PK (source rank j / K, routing rank j % K) of column
   // c0 + i / PK: poll it until it carries this call's tag, then an xor-shuffle tree over the
@@ -260,8 +266,7 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
       wp[u] = nullptr;
       w[u] = 0ull;
       if (i < total) {
-        const int j = i % PK;
-        wp[u] = tp_slot(f, f.tp_rank, j / K, j % K, c0 + i / PK);
+        wp[u] = slots + (long long)c0 * PK + i;
         w[u] = ld_relaxed_sys_u64(wp[u]);
       }
     }
@@ -280,7 +285,7 @@ __device__ __forceinline__ void tp_reduce_epilogue(const FusedArgs& f, int b, in
       const int i = base + u * nthr + ctid;
       float v = wp[u] ? __uint_as_float((uint32_t)w[u]) : 0.f;
       for (int o = 1; o < PK; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (i < total && i % PK == 0) f.yout[c0 + i / PK] = v;
+      if (i < total && i % PK == 0) yout[c0 + i / PK] = v;
     }
   }
   if (ts && ctid == 0) ts[21] = globaltimer();
@@ -314,6 +319,40 @@ __device__ __forceinline__ void record_event(const FusedArgs& f, int* evn, int b
     f.ev[((long long)b * kEvPerCta + i) * 2] = globaltimer();
     f.ev[((long long)b * kEvPerCta + i) * 2 + 1] = (unsigned long long)bytes | ((unsigned long long)phase << 32);
   }
+}
+
+// Paths a single-GPU all-hit decode step never takes live out of line: the kernel is sensitive
+// to its instruction footprint (~1 K never-executed instructions in its body cost 0.2-0.5 us
+// per step in an interleaved A/B). Scalar arguments only (a reference to the kernel's
+// parameter block would be copied to the stack).
+
+// moe_layer_forward_host: x is read straight from the caller's pinned host buffer (one PCIe
+// pass, by CTA 0's consumer threads) into the device staging buffer xd, then published to
+// every CTA (no copy-engine transfer queued in front of the kernel)
+__device__ __noinline__ void xhost_copy(uint16_t* xd, const uint16_t* xhost, uint32_t* xflag, uint32_t xseq, int d,
+                                        int i, int nthr) {
+  for (int k = i; k < (d >> 3); k += nthr) reinterpret_cast<int4*>(xd)[k] = reinterpret_cast<const int4*>(xhost)[k];
+  named_bar_sync(12, nthr);
+  if (i == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(xflag), "r"(xseq) : "memory");
+  }
+}
+
+// MOE_MISS_PULL: this CTA's share of every missed expert's blob, host store -> slot; returns
+// whether it copied anything
+__device__ __noinline__ bool pull_missed(int K, long long slot_bytes, const uint8_t* const* hblob,
+                                         const uint8_t* const* sbase, const int* swait, const int* shost,
+                                         const int* sexp, int ctid, int nthr) {
+  bool any = false;
+  for (int r = 0; r < K; ++r) {
+    if (!swait[r] || shost[r]) continue;
+    any = true;
+    long long u0, u1;
+    pull_share(slot_bytes, blockIdx.x, gridDim.x, &u0, &u1);
+    pull_copy(const_cast<uint8_t*>(sbase[r]), hblob[sexp[r]], u0, u1, ctid, nthr);
+  }
+  return any;
 }
 
 constexpr int kChunkA = 2;     // phase A rows per tail claim
@@ -473,19 +512,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   if (TS(f) && threadIdx.x == 0) TS(f)[b * kTsPerCta + 8] = globaltimer();
   DirState ds;
   if (warp == kRouterWarp) ds = dir_load(ra, lane);  // the router's directory loads in flight
-  if (f.xhost && b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + nthr) {
-    // moe_layer_forward_host: x is read straight from the caller's pinned host buffer (one
-    // PCIe pass, by CTA 0) into the device staging buffer a.x, then published to every CTA
-    // (no copy-engine transfer queued in front of the kernel)
-    const int i = threadIdx.x - 32;
-    for (int k = i; k < (d >> 3); k += nthr)
-      reinterpret_cast<int4*>(const_cast<uint16_t*>(a.x))[k] = reinterpret_cast<const int4*>(f.xhost)[k];
-    named_bar_sync(12, nthr);
-    if (i == 0) {
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f.xflag), "r"(f.xseq) : "memory");
-    }
-  }
+  if (f.xhost && b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + nthr)
+    xhost_copy(const_cast<uint16_t*>(a.x), f.xhost, f.xflag, f.xseq, d, threadIdx.x - 32, nthr);
   if (threadIdx.x == 0) {                    // (host entry: wait for CTA 0's copy of x first)
     const unsigned long long t0 = globaltimer();
     while (f.xhost && (int)(ld_acquire_u32(f.xflag) - f.xseq) < 0) {
@@ -553,14 +581,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       // before any phase-A row is consumed (the producer streams resident experts meanwhile
       // and waits for every CTA's share before its first row of a pulled expert)
       mbar_wait(&rbar, 0);
-      bool any = false;
-      for (int r = 0; r < K; ++r) {
-        if (!swait[r] || shost[r]) continue;
-        any = true;
-        long long u0, u1;
-        pull_share(a.slot_bytes, b, G, &u0, &u1);
-        pull_copy(const_cast<uint8_t*>(sbase[r]), ra.hblob[sexp[r]], u0, u1, ctid, nthr);
-      }
+      const bool any = pull_missed(K, a.slot_bytes, ra.hblob, sbase, swait, shost, sexp, ctid, nthr);
       if (any) named_bar_sync(kPullBar, nthr);  // (uniform: every consumer read the same route)
       // one arrival per CTA and call (the counter's target is (calls + 1) * G); a release only
       // when this CTA copied bytes (a gpu-scope release costs microseconds here)
@@ -1153,7 +1174,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
       else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
     }
   }
-  if (f.tpP > 0) tp_reduce_epilogue(f, b, G, ctid, nthr);
+  if (f.tpP > 0)
+    tp_reduce_epilogue(f.peer[f.tp_rank], f.tpP, K, d, f.tp_calls, f.yout, TS(f) ? TS(f) + b * kTsPerCta : nullptr, b, G,
+                       ctid, nthr);
   if (f.donef) {  // host-buffer entry point: this CTA's slice of y is in host memory
     named_bar_sync(kPullBar, nthr);
     if (ctid == 0) {
