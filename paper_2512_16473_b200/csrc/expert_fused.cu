@@ -227,18 +227,19 @@ __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsign
 // order (K = 2: (v[p][0] + v[p][1]) per source rank, then pairs of ranks): y is
 // bit-identical on every rank.
 // Slots are double-buffered by call parity: a rank one call ahead writes the other half.
-__device__ __forceinline__ unsigned long long* tp_slot(const FusedArgs& f, int p, int src, int r, int c) {
-  const int P = f.tpP, K = f.e.K, d = f.e.d, par = (int)(f.tp_calls & 1);
-  // [parity][column][source rank][routing rank]: the P*K words a receiver sums are contiguous
-  return reinterpret_cast<unsigned long long*>(f.peer[p] + kTpSlotOff) + (((long long)par * d + c) * P + src) * K + r;
-}
-__device__ __forceinline__ unsigned long long tp_tag(const FusedArgs& f) {
-  return (unsigned long long)(uint32_t)(f.tp_calls + 1) << 32;
-}
-// term w_r * o_r[c] of this rank -> every rank's slot
-__device__ __forceinline__ void tp_push(const FusedArgs& f, int r, int c, float v) {
-  const unsigned long long w = tp_tag(f) | __float_as_uint(v);
-  for (int p = 0; p < f.tpP; ++p) st_relaxed_sys_u64(tp_slot(f, p, f.tp_rank, r, c), w);
+// Exchange slot layout ("tp_slot"): [parity][column][source rank][routing rank] of 8-byte
+// words at kTpSlotOff of each rank's buffer — the P*K words a receiver sums are contiguous;
+// the tag is (call number + 1) << 32.
+// term w_r * o_r[c] of this rank -> every rank's slot (tp_slot's layout). Out of line with
+// scalar arguments — the peers' buffers from a shared-memory copy — so that a single-GPU
+// step's phase-B loop carries none of its code.
+__device__ __noinline__ void tp_push(uint8_t* const* peer, int P, int rank, unsigned long long tp_calls, int K, int d,
+                                     int r, int c, float v) {
+  const unsigned long long w = ((unsigned long long)(uint32_t)(tp_calls + 1) << 32) | __float_as_uint(v);
+  const int par = (int)(tp_calls & 1);
+  for (int p = 0; p < P; ++p)
+    st_relaxed_sys_u64(reinterpret_cast<unsigned long long*>(peer[p] + kTpSlotOff) + (((long long)par * d + c) * P + rank) * K + r,
+                       w);
 }
 // (out of line with scalar arguments: a single-GPU step never runs it; it reads only this
 // rank's own exchange buffer `own`)
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
   __shared__ __align__(8) uint64_t hbarK[kMaxFusedK];     // merged phase B: h_r landed and settled (router warp)
   __shared__ __align__(8) uint64_t hrawK[kMaxFusedK];     // merged phase B: h_r's bulk copy landed
   __shared__ __align__(8) uint64_t ybar;                  // segmented phase B: every CTA's y slice zeroed
+  __shared__ uint8_t* speer[8];                           // TP: the ranks' exchange buffers (tp_push)
   __shared__ int evn;                                     // debug: stage events recorded this call
   __shared__ volatile int slastA;                         // phase-A items this CTA issued (once known)
   __shared__ __align__(8) uint64_t pairbar[kMaxNS / 2];  // merged phase B: pair u's even stage left phase A
@@ -504,6 +506,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     }
   }
   if (threadIdx.x == 32) ra = f.r;  // kernel parameters -> shared memory before the PDL wait
+  if (threadIdx.x < 8 && f.tpP > 0) speer[threadIdx.x] = f.peer[threadIdx.x];
   __syncthreads();          // mbarrier inits and routing arguments visible
   const int nwc = kWarpsPerStage * NS;
   // Programmatic dependent launch: the previous call's kernel (cache directory, counters,
@@ -1139,7 +1142,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
           float o = 0.f;
           if (lane < nr) o = ((pb[4 * lane] + pb[4 * lane + 1]) + pb[4 * lane + 2]) + pb[4 * lane + 3];
           if (lane < nr) {
-            if (f.tpP > 0) tp_push(f, r, c + lane, w * o);  // f3 / LL: straight to every rank
+            if (f.tpP > 0) tp_push(speer, f.tpP, f.tp_rank, f.tp_calls, K, d, r, c + lane, w * o);  // f3 / LL
             else if (K == 1) a.y[c + lane] = w * o;
             else red_add_f32(a.y + c + lane, w * o);  // K == 2: 0 + a + b is order-independent
           }
@@ -1169,7 +1172,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     const float* o = a.host_out + (size_t)r * d;
     for (int c = c0 + ctid; c < c1; c += nthr) {
       const float v = w * __ldcg(o + c);
-      if (f.tpP > 0) tp_push(f, r, c, v);
+      if (f.tpP > 0) tp_push(speer, f.tpP, f.tp_rank, f.tp_calls, K, d, r, c, v);
       else if (K == 1) a.y[c] = v;
       else red_add_f32(a.y + c, v);  // K == 2: 0 + a + b is order-independent
     }
