@@ -41,6 +41,20 @@
 #include "pull.cuh"
 #include "route_core.cuh"
 
+// Compiled twice: here with the FHFMA form of the gate GEMV (expert_fused_kernel), and from
+// expert_fused_mma.cu with MOE_FUSED_MMA_GATE = 1 and its tensor-core form
+// (expert_fused_mma_kernel, gate_mma_form(n, d): 9-16 experts). Two translation units so
+// that neither kernel carries the other's code: the kernel pays for every instruction in its
+// cold paths, and a change of its code layout alone measured 0.1-0.25 us on some shapes.
+#ifndef MOE_FUSED_MMA_GATE
+#define MOE_FUSED_MMA_GATE 0
+#endif
+#if MOE_FUSED_MMA_GATE
+#define MOE_FUSED_KERNEL expert_fused_mma_kernel
+#else
+#define MOE_FUSED_KERNEL expert_fused_kernel
+#endif
+
 namespace moe {
 namespace {
 
@@ -401,7 +415,7 @@ __device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct)
 // has moved past segment A_r (the next segment's first row, or kEnd); each stage's single
 // h writer publishes its own rows then (release RED on bar[r]). B_o0 starts only after A_o1 has streamed, so its
 // wait on bar[o0] is normally already satisfied: the grid-wide dependency costs no HBM time.
-__global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedArgs f) {
+__global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs f) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ const uint8_t* sbase[kMaxFusedK];
   __shared__ float swgt[kMaxFusedK];
@@ -543,6 +557,20 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
     // order by the router warp (deterministic).
     mbar_wait(&gbar, 0);
     if (pm && threadIdx.x == 32) pm[0] = clock64();
+#if MOE_FUSED_MMA_GATE
+    {
+      // 9-16 gate rows: the tensor-core form of the shared order (gate_gemv.cuh), virtual
+      // warp = consumer warp
+      const int g = lane >> 2, c4 = lane & 3;
+      const bool hi = g + 8 < n;
+      const float2 z = gate_mma_warp(ring + (size_t)g * gstride + 4 * c4,
+                                     ring + (size_t)(hi ? g + 8 : g) * gstride + 4 * c4, xh + 4 * c4, d >> 4, cw, nwc);
+      if (c4 == 0) {
+        zpart[cw * n + g] = z.x;
+        if (hi) zpart[cw * n + g + 8] = z.y;
+      }
+    }
+#else
     {
       const int nch = d >> 3;                       // 16-B chunks per row
       const int4* xq = reinterpret_cast<const int4*>(xh);
@@ -577,6 +605,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
         if ((lane & 3) == 0 && e < n) zpart[cw * n + e] = z;
       }
     }
+#endif
     if (pm && threadIdx.x == 32) pm[2] = clock64();
     named_bar_arrive(kRouteBar, nthr + 32);  // partial logits ready; on to phase A
     if (f.r.miss_mode == MOE_MISS_PULL) {
@@ -1197,23 +1226,38 @@ __global__ void __launch_bounds__(kThreadsF, 1) expert_fused_kernel(const FusedA
 
 }  // namespace
 
+#if MOE_FUSED_MMA_GATE
+cudaError_t fused_mma_kernel_attrs(int threads, size_t smem, int* blocks_per_sm) {
+  if (blocks_per_sm) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, expert_fused_mma_kernel, threads, smem);
+  cudaFuncAttributes fa;
+  const cudaError_t e = cudaFuncGetAttributes(&fa, expert_fused_mma_kernel);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(expert_fused_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxDynSmem);
+}
+cudaError_t launch_expert_fused_mma(const cudaLaunchConfig_t& cfg, const FusedArgs& f) {
+  return cudaLaunchKernelEx(&cfg, expert_fused_mma_kernel, f);
+}
+#else
+
 // CTAs of the fused kernel wait on each other (h publication), so the whole grid (one CTA
 // per SM) must be resident at once: check that one CTA of this plan fits on an SM.
 int fused_blocks_per_sm(const FusedPlan& p) {
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, expert_fused_kernel, p.threads, p.smem) != cudaSuccess) {
+  int nb = 0, nbm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, expert_fused_kernel, p.threads, p.smem) != cudaSuccess ||
+      fused_mma_kernel_attrs(p.threads, p.smem, &nbm) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  return nb;
+  return min(nb, nbm);
 }
 
 cudaError_t preload_fused_kernels() {
   cudaFuncAttributes fa;
   cudaError_t e = cudaFuncGetAttributes(&fa, expert_fused_kernel);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(expert_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kFusedMaxDynSmem);
+  e = cudaFuncSetAttribute(expert_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFusedMaxDynSmem);
+  if (e != cudaSuccess) return e;
+  return fused_mma_kernel_attrs(0, 0, nullptr);
 }
 
 bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p) {
@@ -1314,7 +1358,9 @@ cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
+  if (gate_mma_form(f.r.n, f.e.d)) return launch_expert_fused_mma(cfg, f);
   return cudaLaunchKernelEx(&cfg, expert_fused_kernel, f);
 }
 
+#endif  // MOE_FUSED_MMA_GATE
 }  // namespace moe

@@ -162,6 +162,10 @@ bool plan_fused(int d, int ffr, int n, int K, int grid, FusedPlan* p);
 cudaError_t launch_expert_fused(const FusedArgs& f, const FusedPlan& p, int grid, cudaStream_t s, bool pdl, bool coop);
 cudaError_t preload_fused_kernels();
 int fused_blocks_per_sm(const FusedPlan& p);
+// the fused kernel with the gate GEMV's tensor-core form (expert_fused_mma.cu): occupancy
+// (blocks_per_sm != null) or attribute preload; launch
+cudaError_t fused_mma_kernel_attrs(int threads, size_t smem, int* blocks_per_sm);
+cudaError_t launch_expert_fused_mma(const cudaLaunchConfig_t& cfg, const FusedArgs& f);
 
 cudaError_t launch_route_probe(const RouteArgs& a, cudaStream_t s, bool pdl);
 

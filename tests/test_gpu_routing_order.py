@@ -9,7 +9,8 @@ reflection-symmetric), so z_0 = z_1 = z_2 in exact arithmetic and only fp32 roun
 i.e. the summation order — decides which two of the three are selected and in which rank
 order. The other gate rows are scaled down so that they never compete. Decode (fused
 kernel), decode (split router) and prefill must produce the identical trace and gate-weight
-bits on every token."""
+bits on every token — with 8 experts (the FHFMA form of the shared order) and with 16 (its
+tensor-core form, gate_mma_form)."""
 import numpy as np
 import pytest
 
@@ -22,9 +23,10 @@ pytestmark = pytest.mark.gpu
 T = 96
 
 
-def _tied_model():
-    # d = 4096 (Mixtral's model width: fp32 rounding of 4096-term sums is common), small experts
-    L, d, ff, n, K = 2, 4096, 128, 8, 2
+def _tied_model(n):
+    # d = 4096 (Mixtral's and Phi's model width: fp32 rounding of 4096-term sums is common),
+    # small experts
+    L, d, ff, K = 2, 4096, 128, 2
     hm = harness.host_model(L, d, ff, n, K)
     rng = np.random.default_rng(7)
     for l in range(L):
@@ -81,8 +83,9 @@ def _prefill(hm, x):
     return tr[np.lexsort((tr["rank"], tr["layer"], tr["token"]))]
 
 
-def test_near_tied_logits_route_identically_on_every_path(monkeypatch):
-    hm, x = _tied_model()
+@pytest.mark.parametrize("n", [8, 16])
+def test_near_tied_logits_route_identically_on_every_path(monkeypatch, n):
+    hm, x = _tied_model(n)
     fused = _decode(hm, x, monkeypatch, split=False)
     split = _decode(hm, x, monkeypatch, split=True)
     pre = _prefill(hm, x)
