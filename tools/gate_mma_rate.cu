@@ -5,6 +5,9 @@
 //   mode 1  mma.sync m16n8k16 bf16 -> fp32 (legacy HMMA), warp w takes k-blocks w, w + 20, ...,
 //           A fragments by 32-bit shared loads, B = x in every column
 //   mode 2  as 1 with two accumulators (even / odd k-blocks of the warp) summed at the end
+//   mode 3  (8 experts) paired k-blocks: rows 0-7 = the experts at the warp's k-block 2i,
+//           rows 8-15 = the same experts at k-block 2i + 1, B column 0 / 1 = x at those
+//           k-blocks; z = D[e][0] + D[e + 8][1]: every MMA does 16 useful rows
 // Prints the median CTA's cycles and the max relative error against an fp64 host GEMV.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gate_mma_rate tools/gate_mma_rate.cu
 #include <cuda_runtime.h>
@@ -90,6 +93,25 @@ __global__ void __launch_bounds__(T, 1) gemv(const uint16_t* Wg, const uint16_t*
         const int e = e0 + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
         if ((lane & 3) == 0 && e < n) zpart[warp * 16 + e] = zz;
       }
+    } else if (MODE == 3) {
+      const int g = lane >> 2, c = lane & 3;
+      const uint8_t* r0 = sm + (size_t)g * gstride + 4 * c;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int nkb = d >> 4;
+      for (int kb = warp; kb < nkb; kb += 2 * W) {
+        const int kb2 = kb + W;
+        const bool two = kb2 < nkb;
+        const int o = kb * 32, o2 = (two ? kb2 : kb) * 32;
+        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0 + o);
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(r0 + o + 16);
+        const uint32_t a1 = two ? *reinterpret_cast<const uint32_t*>(r0 + o2) : 0u;
+        const uint32_t a3 = two ? *reinterpret_cast<const uint32_t*>(r0 + o2 + 16) : 0u;
+        const int ob = g == 1 ? o2 : o;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xs + 4 * c + ob);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xs + 4 * c + ob + 16);
+        mma16816(acc, a0, a1, a2, a3, b0, b1);
+      }
+      if (c == 0) zpart[warp * 16 + g] = acc[0] + acc[3];
     } else {
       const int g = lane >> 2, c = lane & 3;
       const uint8_t* r0 = sm + (size_t)g * gstride + 4 * c;
@@ -140,7 +162,7 @@ static float bf2f(uint16_t v) {
 
 int main() {
   const int G = 148;
-  const int shapes[2][2] = {{8, 6144}, {16, 4096}};
+  const int shapes[3][2] = {{8, 6144}, {8, 4096}, {16, 4096}};
   for (auto& sh : shapes) {
     const int n = sh[0], d = sh[1];
     std::vector<uint16_t> hw((size_t)n * d), hx(d);
@@ -161,8 +183,9 @@ int main() {
     cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
     const int smem = 16 * (2 * d + 16) + 2 * d + W * 16 * 4;
-    for (int mode = 0; mode < 3; ++mode) {
-      auto k = mode == 0 ? gemv<0> : mode == 1 ? gemv<1> : gemv<2>;
+    for (int mode = 0; mode < 4; ++mode) {
+      if (mode == 3 && n > 8) continue;
+      auto k = mode == 0 ? gemv<0> : mode == 1 ? gemv<1> : mode == 2 ? gemv<2> : gemv<3>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       k<<<G, T, smem>>>(dw, dx, d, n, dout, dc);
       k<<<G, T, smem>>>(dw, dx, d, n, dout, dc);
