@@ -522,10 +522,13 @@ def test_prefill_other_baseline_shapes_sampled(name, warm, T):
 
 
 @pytest.mark.parametrize("L,d,ff,n,K,M,T", [(2, 72, 40, 32, 1, 2, 30), (2, 136, 64, 12, 1, 3, 24),
-                                            (3, 4104, 64, 8, 2, 4, 12)])
+                                            (3, 4104, 64, 8, 2, 4, 12), (2, 256, 96, 12, 2, 5, 16),
+                                            (2, 4096, 64, 9, 2, 9, 12), (2, 48, 32, 16, 2, 16, 16)])
 def test_fused_path_odd_shapes(L, d, ff, n, K, M, T):
     """The one-kernel step on shapes off its fast grid: K = 1 (store combine), d % 16 == 8
-    (half a last tensor-core k-step), n = 32 gate rows, d > 4096 (two k-steps per lane)."""
+    (half a last tensor-core k-step), n = 32 gate rows, d > 4096 (two k-steps per lane); the
+    gate GEMV's tensor-core form (9-16 experts, d % 16 == 0) with rows 12-15 / 9-15 of the MMA
+    absent, and with fewer k-blocks (3) than consumer warps."""
     hm = harness.host_model(L, d, ff, n, K)
     x, ranked = harness.hidden_states(hm, T, "paper")
     ref = _oracle_run(hm, x, N=L, M=M)

@@ -9,8 +9,8 @@ reflection-symmetric), so z_0 = z_1 = z_2 in exact arithmetic and only fp32 roun
 i.e. the summation order — decides which two of the three are selected and in which rank
 order. The other gate rows are scaled down so that they never compete. Decode (fused
 kernel), decode (split router) and prefill must produce the identical trace and gate-weight
-bits on every token — with 8 experts (the FHFMA form of the shared order) and with 16 (its
-tensor-core form, gate_mma_form)."""
+bits on every token — with 8 experts (the FHFMA form of the shared order) and with 12 and 16
+(its tensor-core form, gate_mma_form)."""
 import numpy as np
 import pytest
 
@@ -83,7 +83,7 @@ def _prefill(hm, x):
     return tr[np.lexsort((tr["rank"], tr["layer"], tr["token"]))]
 
 
-@pytest.mark.parametrize("n", [8, 16])
+@pytest.mark.parametrize("n", [8, 12, 16])
 def test_near_tied_logits_route_identically_on_every_path(monkeypatch, n):
     hm, x = _tied_model(n)
     fused = _decode(hm, x, monkeypatch, split=False)
