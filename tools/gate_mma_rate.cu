@@ -8,6 +8,9 @@
 //   mode 3  (8 experts) paired k-blocks: rows 0-7 = the experts at the warp's k-block 2i,
 //           rows 8-15 = the same experts at k-block 2i + 1, B column 0 / 1 = x at those
 //           k-blocks; z = D[e][0] + D[e + 8][1]: every MMA does 16 useful rows
+//   mode 4  as 1 with the k index permuted inside each block of 16 (MMA k-pair 2c <-> columns
+//           4c, 4c+1, k-pair 2c+8 <-> 4c+2, 4c+3): A and B fragments by 64-bit shared loads,
+//           3 loads per MMA instead of 6 (same sum, another order)
 // Prints the median CTA's cycles and the max relative error against an fp64 host GEMV.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gate_mma_rate tools/gate_mma_rate.cu
 #include <cuda_runtime.h>
@@ -92,6 +95,24 @@ __global__ void __launch_bounds__(T, 1) gemv(const uint16_t* Wg, const uint16_t*
         zz += __shfl_xor_sync(0xffffffffu, zz, 1);
         const int e = e0 + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
         if ((lane & 3) == 0 && e < n) zpart[warp * 16 + e] = zz;
+      }
+    } else if (MODE == 4) {
+      const int g = lane >> 2, c = lane & 3;
+      const uint8_t* r0 = sm + (size_t)g * gstride + 8 * c;
+      const uint8_t* r1 = sm + (size_t)(g + 8) * gstride + 8 * c;
+      const uint8_t* xp = xs + 8 * c;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int nkb = d >> 4;
+      for (int kb = warp; kb < nkb; kb += W) {
+        const int o = kb * 32;
+        const uint2 a02 = *reinterpret_cast<const uint2*>(r0 + o);
+        const uint2 a13 = n > 8 ? *reinterpret_cast<const uint2*>(r1 + o) : make_uint2(0u, 0u);
+        const uint2 b01 = *reinterpret_cast<const uint2*>(xp + o);
+        mma16816(acc, a02.x, a13.x, a02.y, a13.y, b01.x, b01.y);
+      }
+      if (c == 0) {
+        zpart[warp * 16 + g] = acc[0];
+        if (g + 8 < n) zpart[warp * 16 + g + 8] = acc[2];
       }
     } else if (MODE == 3) {
       const int g = lane >> 2, c = lane & 3;
@@ -183,9 +204,9 @@ int main() {
     cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice);
     cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
     const int smem = 16 * (2 * d + 16) + 2 * d + W * 16 * 4;
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
       if (mode == 3 && n > 8) continue;
-      auto k = mode == 0 ? gemv<0> : mode == 1 ? gemv<1> : mode == 2 ? gemv<2> : gemv<3>;
+      auto k = mode == 0 ? gemv<0> : mode == 1 ? gemv<1> : mode == 2 ? gemv<2> : mode == 3 ? gemv<3> : gemv<4>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       k<<<G, T, smem>>>(dw, dx, d, n, dout, dc);
       k<<<G, T, smem>>>(dw, dx, d, n, dout, dc);
