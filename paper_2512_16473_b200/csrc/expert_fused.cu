@@ -221,6 +221,14 @@ __device__ __noinline__ void settle_h(float* dst, const float* src, int n, int t
 }
 
 // spin until *p >= target (acquire); 60 s -> trap
+// One stage's publication of h_r (its rows written with plain stores; readers settle what has
+// not landed): the CTA's NS stages count in shared memory and the last of them adds NS to the
+// grid-wide counter in one relaxed RED — G instead of G x NS same-address atomics per expert,
+// which the L2 serialises (a tiny step saw h complete ~2 us after the last publication)
+__device__ __forceinline__ void publish_h(unsigned* spub, unsigned long long* bar, int NS) {
+  if (atomicAdd(spub, 1u) == (unsigned)NS - 1u) red_relaxed_add_u64(bar, (unsigned long long)NS);
+}
+
 __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target) {
   if (ld_acquire_u64(p) >= target) return;
   const unsigned long long t0 = globaltimer();
@@ -431,6 +439,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
   __shared__ uint8_t* speer[8];                           // TP: the ranks' exchange buffers (tp_push)
   __shared__ int evn;                                     // debug: stage events recorded this call
   __shared__ volatile int slastA;                         // phase-A items this CTA issued (once known)
+  __shared__ unsigned spub[kMaxFusedK];                   // stages that published h_r (publish_h)
   __shared__ __align__(8) uint64_t pairbar[kMaxNS / 2];  // merged phase B: pair u's even stage left phase A
   __shared__ RouteArgs ra;                                // routing arguments (read once, off the critical path)
   const ExpertArgs& a = f.e;
@@ -493,6 +502,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
     mbar_init(&wbar, 32);
     mbar_init(&ybar, 1);
     evn = 0;
+    for (int r = 0; r < kMaxFusedK; ++r) spub[r] = 0u;
     slastA = 0x7fffffff;
     for (int r = 0; r < kMaxFusedK; ++r) {
       mbar_init(hbarK + r, 32);             // merged: every router lane after settling its words
@@ -1022,7 +1032,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
       if (half == 0 && lane == 0)
         for (; pubseg < si; ++pubseg) {
           if (TS(f) && sA == 0 && pubseg == 0) TS(f)[b * kTsPerCta + 39] = globaltimer();
-          red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+          publish_h(spub + sorder[pubseg], f.bar + 16 * sorder[pubseg], NS);
           if (TS(f) && sA == 0 && pubseg == 0) TS(f)[b * kTsPerCta + 40] = globaltimer();
         }
       if (TS(f) && first && cw == 0 && lane == 0) TS(f)[b * kTsPerCta + 2] = globaltimer();
@@ -1053,13 +1063,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
         // this stage's last phase-A row (known once the producer issued its last one): publish
         // every segment now instead of at the next item (end marker or W2 rows)
         if (ti + NS >= slastA)
-          for (const int nseg = snseg; pubseg < nseg; ++pubseg) red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+          for (const int nseg = snseg; pubseg < nseg; ++pubseg) publish_h(spub + sorder[pubseg], f.bar + 16 * sorder[pubseg], NS);
       }
     }
     if (half == 0 && lane == 0)            // the rest of this stage's segments
       for (const int nseg = snseg; pubseg < nseg; ++pubseg) {
         if (TS(f) && sA == 0) TS(f)[b * kTsPerCta + 41 + 2 * pubseg] = globaltimer();
-        red_relaxed_add_u64(f.bar + 16 * sorder[pubseg], 1ull);
+        publish_h(spub + sorder[pubseg], f.bar + 16 * sorder[pubseg], NS);
         if (TS(f) && sA == 0) TS(f)[b * kTsPerCta + 42 + 2 * pubseg] = globaltimer();
       }
     named_bar_sync(2 + sA, 64);
