@@ -420,9 +420,11 @@ __device__ __forceinline__ RowSched make_sched(int total, int b, int G, int pct)
 //
 // Work order (all CTAs, no group split): phase A of every device-computed expert in turn
 // (A_o0, A_o1), then phase B (B_o0, B_o1). h_r is complete once every stage of every CTA
-// has moved past segment A_r (the next segment's first row, or kEnd); each stage's single
-// h writer publishes its own rows then (release RED on bar[r]). B_o0 starts only after A_o1 has streamed, so its
-// wait on bar[o0] is normally already satisfied: the grid-wide dependency costs no HBM time.
+// has moved past segment A_r (the next segment's first row, its own last row, or kEnd); each
+// stage's single h writer publishes its rows then (publish_h: the CTA's last stage adds NS to
+// bar[r] in one relaxed RED; readers settle words whose plain stores have not landed yet).
+// B_o0 starts only after A_o1 has streamed, so its wait on bar[o0] is normally already
+// satisfied: the grid-wide dependency costs no HBM time.
 __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs f) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ const uint8_t* sbase[kMaxFusedK];
