@@ -78,6 +78,7 @@ constexpr int kRouterWarp = 1 + kWarpsPerStage * kMaxNS;  // warp 0 producer, 1.
 constexpr int kRouteBar = 13;              // named barrier: partial logits -> router warp
 constexpr int kThreadsF = 32 * (kRouterWarp + 1);
 constexpr int kMaxFusedK = 2;             // deterministic combine: 0 + a + b commutes
+static_assert(2 * 2 * kMaxFusedK * kCtrStride == kCtrWords, "work-claim counter layout");
 constexpr int kTsPerCta = kTsStride;      // debug timestamps per CTA (MOE_DEBUG_TS)
 constexpr int kMaxRB = 16;                // phase B: max W2 rows per super-stage
 // back-off of the polls on flags other CTAs set (interleaved A/B: a pure spin was 0.1-0.25 us
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
   const unsigned long long bar_target = (f.calls + 1) * (unsigned long long)G * (unsigned long long)NS;
   float* const hcur = f.hf + (long long)(f.calls & 1) * K * ffr;   // this call's h (relaxed publication)
   // work-claim counters of this call ([A r][B r]); the other parity is zeroed for the next
-  unsigned* ctr = f.ctr + (f.calls & 1) * (2 * kMaxFusedK);
+  unsigned* ctr = f.ctr + (f.calls & 1) * (2 * kMaxFusedK) * kCtrStride;  // (one 128-B line per counter)
   // the ring is free until the route is known: it stages the gate rows and x first
   // gate rows at a padded stride (+16 B: the 8 rows of an MMA fragment hit distinct banks)
   const int gstride = 2 * d + 16;
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
     bulk_g2s(xh, a.x, 2u * d, &xbar, policy_evict_last());
   }
   if (b == 0 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kMaxFusedK)
-    f.ctr[((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32] = 0u;
+    f.ctr[(((f.calls + 1) & 1) * (2 * kMaxFusedK) + threadIdx.x - 32) * kCtrStride] = 0u;
   unsigned long long* pm = TS(f) ? TS(f) + b * kTsPerCta + 24 : nullptr;  // debug marks
   if (cw >= 0 && cw < nwc) {
     // x: one bulk copy into xh (measured faster than per-thread L2 loads of the GEMV's own
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
       unsigned pre = 0u;
       int pre_q = -1;
       auto seg_ctr = [&](int q) -> unsigned* {
-        return q < nseg ? ctr + sorder[q] : ctr + kMaxFusedK + sorder[q - nseg];
+        return ctr + (q < nseg ? sorder[q] : kMaxFusedK + sorder[q - nseg]) * kCtrStride;
       };
       auto seg_chunk = [&](int q) -> unsigned { return q < nseg ? (unsigned)kChunkA : (unsigned)RB; };
       auto first_claim = [&](int q) -> unsigned {
@@ -837,7 +838,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
           else wait_ready(a.ready, sslot[r], sgen[r]);
           asm volatile("fence.proxy.async.global;" ::: "memory");  // generic/DMA writes -> bulk reads
         }
-        unsigned* cA = ctr + r;
+        unsigned* cA = ctr + r * kCtrStride;
         auto issue_a = [&](int j) {
           const int s = t % NS;
           acquire(s);
@@ -940,7 +941,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
         };
         for (int si = 0; si < nseg; ++si) {     // experts in turn, without markers between them
           const int r = sorder[si];
-          unsigned* cB = ctr + kMaxFusedK + r;
+          unsigned* cB = ctr + (kMaxFusedK + r) * kCtrStride;
           unsigned e1 = first_claim(nseg + si);
           for (int c = sbk.s0; c < sbk.s1; c += RB) issue_b(r, c, min(RB, sbk.s1 - c));
           unsigned e2 = atomicAdd(cB, (unsigned)RB);
@@ -966,7 +967,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) MOE_FUSED_KERNEL(const FusedArgs
       for (int si = 0; si < nseg; ++si) {
         const int r = sorder[si];
         const uint8_t* w2 = sbase[r] + w2off;
-        unsigned* cB = ctr + kMaxFusedK + r;
+        unsigned* cB = ctr + (kMaxFusedK + r) * kCtrStride;
         // RB consecutive W2 rows (contiguous in the slot) per super-stage: short rows
         // (small ff_r) would otherwise leave too few bytes in flight per SM
         auto issue_b = [&](int c, int nr) {

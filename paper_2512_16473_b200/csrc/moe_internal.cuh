@@ -13,6 +13,10 @@
 namespace moe {
 
 constexpr int kMaxK = MOE_MAX_EXPERTS;  // K <= n <= 32
+// fused kernel work-claim counters: 2 call parities x (phase A, phase B) x 2 experts, each on
+// its own 128-B line (same-line atomics serialise in one L2 slice)
+constexpr int kCtrStride = 32;
+constexpr int kCtrWords = 2 * 2 * 2 * kCtrStride;
 constexpr int kMailRing = 1024;         // miss-notification mailbox entries (host-mapped)
 constexpr int kStsRing = 64;            // debug step-timestamp records (MOE_DEBUG_TS)
 constexpr int kStsHead = 8;             // router marks per record

@@ -653,7 +653,7 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMemset(c->d_xflag, 0, sizeof(uint32_t)));
   INIT_TRY(cudaMalloc(&c->d_bar, sizeof(unsigned long long) * 16 * kMaxK));
   INIT_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
-  INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * 2 * kMaxK));
+  INIT_TRY(cudaMalloc(&c->d_ctr, sizeof(unsigned) * kCtrWords));
   INIT_TRY(cudaHostAlloc((void**)&c->h_xring, sizeof(uint16_t) * (size_t)d * kMailRing, cudaHostAllocMapped));
   INIT_TRY(cudaHostGetDevicePointer((void**)&c->d_xring, c->h_xring, 0));
   INIT_TRY(cudaHostAlloc((void**)&c->h_hout, sizeof(float) * (size_t)d * kMaxK, cudaHostAllocDefault));
@@ -661,7 +661,7 @@ MOE_API moe_status moe_init(const moe_model_desc* desc, const moe_weights* w, mo
   INIT_TRY(cudaMalloc(&c->d_hflag, sizeof(uint32_t) * kMaxK));
   INIT_TRY(cudaMemset(c->d_hflag, 0, sizeof(uint32_t) * kMaxK));
   INIT_TRY(cudaStreamCreateWithFlags(&c->act_stream, cudaStreamNonBlocking));
-  INIT_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * 2 * kMaxK));
+  INIT_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * kCtrWords));
   {
     const char* path = getenv("MOE_EXPERT_PATH");
     const char* pdl = getenv("MOE_PDL");
@@ -1542,7 +1542,7 @@ static moe_status tp_reset(moe_ctx* c) {
   // the fused kernel's monotonic per-call counters assume a fixed grid: restart them (the
   // grid may have changed in moe_tp_connect_local)
   CUDA_TRY(cudaMemset(c->d_bar, 0, sizeof(unsigned long long) * 16 * kMaxK));
-  CUDA_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * 2 * kMaxK));
+  CUDA_TRY(cudaMemset(c->d_ctr, 0, sizeof(unsigned) * kCtrWords));
   CUDA_TRY(cudaMemset(c->d_hf, 0xff, sizeof(float) * 2 * (size_t)c->K * c->ffr));  // call parity restarts
   CUDA_TRY(cudaDeviceSynchronize());
   c->fused_calls = 0;
